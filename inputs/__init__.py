@@ -1,0 +1,13 @@
+"""Seeded synthetic input generators shared by the oracle tests and the CUDA path.
+
+This package holds NO arithmetic of the method (no chase, no reflector application):
+only a counter-based splitmix64 stream and the recipes that turn it into inputs
+(DESIGN.md §3 "Input recipe").  Both a numpy and a torch implementation of the same
+counter-based generator are provided so device-side generation for the bench is
+bitwise identical to host-side generation for the oracle (tests/test_inputs.py).
+"""
+from .synth import (  # noqa: F401
+    GAMMA, splitmix64_np, uniform_pm1_np, uniform_pm1_torch,
+    band_matrix, synthetic_reflectors, synthetic_q_np, synthetic_q_torch,
+    config_seed, CONFIGS,
+)

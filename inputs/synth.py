@@ -1,0 +1,124 @@
+"""Counter-based splitmix64 generators ("seeded
+splitmix-style generator").
+
+Element t of stream `seed` is splitmix64(seed + (t+1)*GAMMA) — a pure function of
+(seed, t), so any sub-block of any input (a column range of Q, a sampled column) can be
+regenerated independently on host (numpy) or device (torch) with identical bits.
+
+u = (z >> 11) * 2^-53 in [0, 1);  a = 2u - 1 in [-1, 1).
+"""
+import numpy as np
+
+GAMMA = 0x9E3779B97F4A7C15
+_M1 = 0xBF58476D1CE4E5B9
+_M2 = 0x94D049BB133111EB
+_TWO53 = float(2 ** -53)
+
+# Stream tags: independent streams for the different inputs of one config seed.
+TAG_BAND = 0x0
+TAG_HHV = 0x5F1A2B3C4D5E6F70
+TAG_Q = 0x2A7B9C1D3E5F7081
+
+# BASELINE.json configs: name -> (n, nbw, nev); seeds S_i = 1811012770 + i
+CONFIGS = {
+    "C1": (512, 16, 512),
+    "C2": (4096, 32, 4096),
+    "C3": (20000, 64, 20000),
+    "C4": (20000, 64, 2000),
+    "C5": (60000, 64, 30000),
+}
+
+
+def config_seed(i):
+    return 1811012770 + int(i)
+
+
+def splitmix64_np(seed, counters):
+    """splitmix64 output for counters (uint64 array)."""
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + (counters.astype(np.uint64) + np.uint64(1)) * np.uint64(GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(_M1)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(_M2)
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def uniform_pm1_np(seed, counters):
+    z = splitmix64_np(seed, counters)
+    u = (z >> np.uint64(11)).astype(np.float64) * _TWO53
+    return 2.0 * u - 1.0
+
+
+def _s64(x):
+    x &= 0xFFFFFFFFFFFFFFFF
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def uniform_pm1_torch(seed, counters):
+    """Same stream as uniform_pm1_np, computed with torch int64 (wrapping) arithmetic.
+    `counters` is an int64 torch tensor (any device)."""
+    import torch
+    def lsr(z, k):  # logical shift right on int64
+        return (z >> k) & ((1 << (64 - k)) - 1)
+    z = (counters + 1) * _s64(GAMMA) + _s64(seed)
+    z = (z ^ lsr(z, 30)) * _s64(_M1)
+    z = (z ^ lsr(z, 27)) * _s64(_M2)
+    z = z ^ lsr(z, 31)
+    u = lsr(z, 11).to(torch.float64) * _TWO53
+    return 2.0 * u - 1.0
+
+
+def band_matrix(n, nbw, seed):
+    """Random symmetric band matrix, entries i.i.d. uniform [-1,1).
+
+    Returns LAPACK-style lower band storage `band` of shape (nbw+1, n):
+    band[d, c] = B[c+d, c] for c+d < n (zero otherwise).  Draw order: c ascending, then
+    d ascending, skipping c+d >= n without drawing (one draw per stored entry)."""
+    n, nbw = int(n), int(nbw)
+    band = np.zeros((nbw + 1, n), dtype=np.float64)
+    if n == 0:
+        return band
+    cnt = np.minimum(nbw + 1, n - np.arange(n))            # entries drawn in column c
+    off = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+    c_idx = np.repeat(np.arange(n), cnt)
+    d_idx = np.arange(cnt.sum()) - np.repeat(off, cnt)
+    vals = uniform_pm1_np(seed ^ TAG_BAND, np.arange(cnt.sum(), dtype=np.uint64))
+    band[d_idx, c_idx] = vals
+    return band
+
+
+def synthetic_reflectors(R, nbw, seed):
+    """Synthetic Householder reflectors for timing / sampled parity at sizes where the
+    oracle's chase is too slow: v[0] = 1, v[1:] uniform [-1,1),
+    tau = 2/||v||^2 over the full nbw entries (so every truncated reflector is a
+    contraction and every full one orthogonal).  Returns (hh_v (R, nbw) C-order ==
+    nbw x R column-major, hh_tau (R,))."""
+    R, nbw = int(R), int(nbw)
+    v = uniform_pm1_np(seed ^ TAG_HHV, np.arange(R * nbw, dtype=np.uint64)).reshape(R, nbw)
+    v[:, 0] = 1.0
+    tau = 2.0 / np.einsum("ij,ij->i", v, v)
+    return v, tau
+
+
+def synthetic_q_np(n, c0, c1, seed, ldq=None):
+    """Columns [c0, c1) of the synthetic n x nev eigenvector block, uniform [-1,1):
+    element (i, c) = stream(seed^TAG_Q)[c*n + i].  Returns (c1-c0, ldq) C-order array
+    (the row-major view of a column-major n x (c1-c0) block with leading dim ldq)."""
+    ldq = n if ldq is None else ldq
+    out = np.zeros((c1 - c0, ldq), dtype=np.float64)
+    if c1 > c0 and n > 0:
+        cnt = np.arange(c0 * n, c1 * n, dtype=np.uint64)
+        out[:, :n] = uniform_pm1_np(seed ^ TAG_Q, cnt).reshape(c1 - c0, n)
+    return out
+
+
+def synthetic_q_torch(n, c0, c1, seed, ldq=None, device="cpu", chunk_cols=1024):
+    """torch version of synthetic_q_np (bitwise identical), generated on `device`."""
+    import torch
+    ldq = n if ldq is None else ldq
+    out = torch.zeros((c1 - c0, ldq), dtype=torch.float64, device=device)
+    for a in range(c0, c1, chunk_cols):
+        b = min(c1, a + chunk_cols)
+        cnt = torch.arange(a * n, b * n, dtype=torch.int64, device=device)
+        out[a - c0:b - c0, :n] = uniform_pm1_torch(seed ^ TAG_Q, cnt).reshape(b - a, n)
+    return out
