@@ -1,0 +1,142 @@
+/*
+ * elpa_b200.h — B200-native stage-2 eigenvector back-transformation of ELPA's two-stage
+ * symmetric eigensolver (trans_ev_tridi_to_band), FP64, sm_100a only.
+ *
+ * What it computes (PAPER.md = arXiv 1811.01277 source; "P:L" = line L):
+ *   The two-stage solver reduces a symmetric matrix to band form, then the band matrix B
+ *   (half-bandwidth nbw) to tridiagonal T with Householder reflectors
+ *   Q_i = I - beta_i v_i v_i^H that are "never constructed explicitly, but are always
+ *   represented only by the Householder vector v_i" (Sec. 2 after Eq. 4;
+ *   two-stage: P:141-144).  The eigenvectors Vhat of T (Eq. 5) must be
+ *   back-transformed, Vtilde = Q^H Vhat (Eq. 6), and in the two-stage path
+ *   "each eigenvector" is transformed twice.  This library performs the
+ *   first of those two transforms — band <- tridiagonal — for nev eigenvectors:
+ *
+ *       Q  <-  H_0 H_1 ... H_{R-1} Q ,   H_r = I - tau_r v_r v_r^T   (H_{R-1} applied first)
+ *
+ *   Reflector r = (j, m) is the m-th reflector of chase sweep j (the sweep that
+ *   eliminates column j), numbered in generation order (j ascending, then m ascending):
+ *       first row   s = j + 1 + m*nbw        (0-based),
+ *       length      L = min(nbw, n - s)      (it exists iff L >= 2),
+ *       index       r(j,m) = off(j) + m,  off(j) = j + F(n-3) - F(n-3-j),
+ *       F(x) = sum_{t=0}^{x} floor(t/nbw),  R = (n-2) + F(n-3)   (0 if n < 3 or nbw < 2).
+ *   The reading of the chase, order and storage conventions is DESIGN.md §2 (R1-R12).
+ *
+ * Conventions shared by every entry point below
+ *   hh_v   : nbw x R column-major (column r = reflector r's vector, contiguous, nbw doubles).
+ *            Element 0 is treated as 1.0 (LAPACK v_0 = 1; SPEC S:196 — so buffers that keep
+ *            tau in v_0 are accepted); elements >= L are never read.
+ *   hh_tau : R doubles.  tau == 0 is the identity.
+ *   Q      : n x nev column-major with leading dimension ldq (eigenvector c = column c).
+ *            In: eigenvectors of T.  Out: eigenvectors of B (same eigenvalues).  Updated
+ *            in place; rows [n, ldq) of every column are never written.
+ *   Ownership: the caller owns every buffer.  The library keeps no state between calls and
+ *            no persistent allocation; the one-shot entry points take a temporary device
+ *            workspace from cudaMallocAsync/cudaFreeAsync on `stream`.
+ *   Concurrency: calls on distinct streams with distinct buffers may run concurrently (the
+ *            analogue of ELPA's multiple instances).  No host synchronisation
+ *            happens inside the device-pointer entry points.
+ *   Errors: integer codes (the analogue of ELPA's `int *error` out-parameter).
+ *            Validation happens before any device work, in the order of the table in
+ *            DESIGN.md §4; a kernel fault surfaces at the caller's next synchronisation.
+ *            There is no CPU fallback and no slow path for misaligned Q.
+ */
+#ifndef ELPA_B200_H
+#define ELPA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t without including cuda_runtime.h (ABI: a CUstream handle, 0 = legacy default) */
+typedef struct CUstream_st *elpa_b200_stream_t;
+
+enum {
+    ELPA_B200_OK = 0,
+    ELPA_B200_ERR_ARG = -1,    /* n < 0, nbw < 1, nev < 0, nev > n, ldq < max(1,n), bad opts */
+    ELPA_B200_ERR_NULL = -2,   /* a required pointer is NULL (R > 0 and nev > 0) */
+    ELPA_B200_ERR_ALIGN = -3,  /* ldq odd or Q not 16-byte aligned; workspace not 256-byte aligned */
+    ELPA_B200_ERR_DEVICE = -4, /* current device is not compute capability 10.0 (B200, sm_100a) */
+    ELPA_B200_ERR_CUDA = -5,   /* a CUDA runtime call or kernel launch failed */
+    ELPA_B200_ERR_SPACE = -6   /* workspace smaller than elpa_b200_workspace_bytes() */
+};
+
+/* Kernel variants (elpa_b200_opts.kernel). */
+enum {
+    ELPA_B200_KERNEL_AUTO = 0,
+    ELPA_B200_KERNEL_REFERENCE = 1, /* one thread per column, exact reverse generation order,
+                                       no FMA contraction: bitwise equal to the CPU oracle */
+    ELPA_B200_KERNEL_DMMA = 2       /* k = 8 compact-WY groups on FP64 tensor cores (DMMA),
+                                       depth-pipelined row windows; requires nbw % 8 == 0 */
+};
+
+/* Optional tuning knobs (the paper's "numerical blocking parameters of the
+ * back-transformation").  Zero-initialise for automatic choices. */
+typedef struct {
+    int kernel;          /* ELPA_B200_KERNEL_* */
+    int depth_warps;     /* D: chase depths pipelined inside one CTA (1,2,4,8), 0 = auto */
+    int col_warps;       /* CW: warps splitting the CTA's column stripe, 0 = auto */
+    int tiles_per_warp;  /* NCT: 8-column tiles per warp (1,2,4), 0 = auto */
+    int tiles_per_cta;   /* 8-column tiles per CTA (<= CW*NCT), 0 = auto (balance over SMs) */
+} elpa_b200_opts;
+
+/* R(n, nbw): number of reflectors the band->tridiagonal chase produces.
+ * 0 if n < 3 or nbw == 1 (nbw = 1: the input is already tridiagonal);
+ * -1 if n < 0 or nbw < 1. */
+int64_t elpa_hh_count(int64_t n, int64_t nbw);
+
+/* One-shot device call: Q <- H_0 ... H_{R-1} Q, asynchronous on `stream`.
+ * hh_v, hh_tau, Q are device pointers.  Returns ELPA_B200_OK or a negative code.
+ * nev == 0 or R == 0 returns OK without touching memory. */
+int elpa_trans_ev_tridi_to_band(int64_t n, int64_t nbw, int64_t nev,
+                                const double *hh_v, const double *hh_tau,
+                                double *Q, int64_t ldq, elpa_b200_stream_t stream);
+
+/* Same, with tuning options (opts may be NULL = all automatic). */
+int elpa_trans_ev_tridi_to_band_ex(int64_t n, int64_t nbw, int64_t nev,
+                                   const double *hh_v, const double *hh_tau,
+                                   double *Q, int64_t ldq, elpa_b200_stream_t stream,
+                                   const elpa_b200_opts *opts);
+
+/* Host-buffer call (end-to-end path): hh_v, hh_tau, Q are HOST pointers (pinned memory is
+ * fastest).  Copies the inputs to a temporary device workspace on `stream`, runs the
+ * transform, copies Q back and synchronises `stream` before returning. */
+int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev,
+                                     const double *hh_v, const double *hh_tau,
+                                     double *Q, int64_t ldq, elpa_b200_stream_t stream,
+                                     const elpa_b200_opts *opts);
+
+/* Two-phase use (prepare the reflectors once, apply them to many eigenvector blocks):
+ * elpa_b200_workspace_bytes  -> bytes of device workspace for the prepared reflectors
+ *                               (0 when the chosen kernel needs none); -1 on bad args.
+ * elpa_b200_prepare          -> re-lays hh_v/hh_tau into per-group tensor-core fragments
+ *                               plus the k x k compact-WY factor of every group.
+ * elpa_b200_apply_prepared   -> Q <- H_0 ... H_{R-1} Q from the prepared workspace (the
+ *                               REFERENCE kernel reads hh_v/hh_tau directly; pass them). */
+int64_t elpa_b200_workspace_bytes(int64_t n, int64_t nbw, const elpa_b200_opts *opts);
+int elpa_b200_prepare(int64_t n, int64_t nbw, const double *hh_v, const double *hh_tau,
+                      void *workspace, size_t workspace_bytes, elpa_b200_stream_t stream,
+                      const elpa_b200_opts *opts);
+int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev,
+                             const double *hh_v, const double *hh_tau,
+                             const void *workspace, size_t workspace_bytes,
+                             double *Q, int64_t ldq, elpa_b200_stream_t stream,
+                             const elpa_b200_opts *opts);
+
+/* Describe the launch the library would make for (n, nbw, nev, opts): writes
+ * "kernel=... D=.. CW=.. NCT=.. tiles_per_cta=.. grid=.. block=.. smem=.." into buf.
+ * Returns the number of kernel launches one elpa_trans_ev_tridi_to_band call makes, or a
+ * negative code. */
+int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *opts,
+                       char *buf, size_t buflen);
+
+/* Static description of an error code. */
+const char *elpa_b200_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELPA_B200_H */

@@ -1,0 +1,178 @@
+"""paper_1811_01277_b200 — B200-native trans_ev_tridi_to_band (ELPA two-stage eigensolver,
+arXiv 1811.01277).  Thin ctypes binding over the C-ABI library libelpa_b200.so
+(include/elpa_b200.h): argument marshalling only — every step of the path runs in the
+library's sm_100a kernels.  There is no CPU fallback: importing fails loudly if the
+library cannot be loaded.
+
+Tensors: Q is a float64 CUDA tensor of shape (nev, ldq) — the row-major view of the
+column-major n x nev eigenvector block (row c = eigenvector c, first n entries used).
+hh_v is (R, nbw) (== nbw x R column-major), hh_tau is (R,).
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libelpa_b200.so")
+
+OK, ERR_ARG, ERR_NULL, ERR_ALIGN, ERR_DEVICE, ERR_CUDA, ERR_SPACE = 0, -1, -2, -3, -4, -5, -6
+KERNEL_AUTO, KERNEL_REFERENCE, KERNEL_DMMA = 0, 1, 2
+
+
+def _load():
+    if not os.path.exists(_SO):
+        from . import build as _build
+        _build.build()
+    lib = ctypes.CDLL(_SO)
+    i64, p, i32, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    lib.elpa_hh_count.restype = i64
+    lib.elpa_hh_count.argtypes = [i64, i64]
+    lib.elpa_trans_ev_tridi_to_band.restype = i32
+    lib.elpa_trans_ev_tridi_to_band.argtypes = [i64, i64, i64, p, p, p, i64, p]
+    for f in (lib.elpa_trans_ev_tridi_to_band_ex, lib.elpa_trans_ev_tridi_to_band_host):
+        f.restype = i32
+        f.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
+    lib.elpa_b200_workspace_bytes.restype = i64
+    lib.elpa_b200_workspace_bytes.argtypes = [i64, i64, p]
+    lib.elpa_b200_prepare.restype = i32
+    lib.elpa_b200_prepare.argtypes = [i64, i64, p, p, p, sz, p, p]
+    lib.elpa_b200_apply_prepared.restype = i32
+    lib.elpa_b200_apply_prepared.argtypes = [i64, i64, i64, p, p, p, sz, p, i64, p, p]
+    lib.elpa_b200_describe.restype = i32
+    lib.elpa_b200_describe.argtypes = [i64, i64, i64, p, ctypes.c_char_p, sz]
+    lib.elpa_b200_strerror.restype = ctypes.c_char_p
+    lib.elpa_b200_strerror.argtypes = [i32]
+    return lib
+
+
+_lib = _load()
+LIBRARY_PATH = _SO
+
+
+class Opts(ctypes.Structure):
+    """elpa_b200_opts (include/elpa_b200.h)."""
+    _fields_ = [("kernel", ctypes.c_int), ("depth_warps", ctypes.c_int), ("col_warps", ctypes.c_int),
+                ("tiles_per_warp", ctypes.c_int), ("tiles_per_cta", ctypes.c_int)]
+
+
+class ElpaB200Error(RuntimeError):
+    def __init__(self, code, where=""):
+        self.code = code
+        super().__init__(f"{where}: {code} ({strerror(code)})")
+
+
+def strerror(code):
+    return _lib.elpa_b200_strerror(int(code)).decode()
+
+
+def hh_count(n, nbw):
+    return int(_lib.elpa_hh_count(int(n), int(nbw)))
+
+
+def _opts_ptr(opts):
+    if opts is None:
+        return None, None
+    if isinstance(opts, dict):
+        opts = Opts(**opts)
+    return opts, ctypes.byref(opts)
+
+
+def _stream_handle(stream, device):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(rc, where):
+    if rc != OK:
+        raise ElpaB200Error(rc, where)
+
+
+def _dev_ptr(t, name):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
+        raise TypeError(f"{name} must be a float64 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _q_ldq(Q):
+    if Q.dim() != 2 or Q.stride(1) != 1:
+        raise ValueError("Q must be a (nev, ldq) tensor with unit stride along ldq")
+    return Q.shape[0], (Q.stride(0) if Q.shape[0] > 1 else Q.shape[1])
+
+
+def trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Q, stream=None, opts=None):
+    """Q <- H_0 H_1 ... H_{R-1} Q in place on the GPU (elpa_trans_ev_tridi_to_band[_ex]).
+    Asynchronous on `stream` (default: torch's current stream)."""
+    nev, ldq = _q_ldq(Q)
+    o, op = _opts_ptr(opts)
+    s = _stream_handle(stream, Q.device)
+    args = (int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v"), _dev_ptr(hh_tau, "hh_tau"),
+            _dev_ptr(Q, "Q"), int(ldq), s)
+    rc = _lib.elpa_trans_ev_tridi_to_band(*args) if op is None else \
+        _lib.elpa_trans_ev_tridi_to_band_ex(*args, op)
+    _check(rc, "elpa_trans_ev_tridi_to_band")
+    return Q
+
+
+def trans_ev_tridi_to_band_host(n, nbw, hh_v, hh_tau, Q, stream=None, opts=None):
+    """Host-buffer entry point (elpa_trans_ev_tridi_to_band_host): hh_v, hh_tau, Q are CPU
+    float64 tensors (pinned for speed); Q is updated in place; synchronises `stream`."""
+    import torch
+    for t, nm in ((hh_v, "hh_v"), (hh_tau, "hh_tau"), (Q, "Q")):
+        if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+            raise TypeError(f"{nm} must be a contiguous float64 CPU tensor")
+    nev, ldq = _q_ldq(Q)
+    o, op = _opts_ptr(opts)
+    s = _stream_handle(stream, torch.device("cuda", torch.cuda.current_device()))
+    rc = _lib.elpa_trans_ev_tridi_to_band_host(int(n), int(nbw), int(nev), ctypes.c_void_p(hh_v.data_ptr()),
+                                              ctypes.c_void_p(hh_tau.data_ptr()), ctypes.c_void_p(Q.data_ptr()),
+                                              int(ldq), s, op)
+    _check(rc, "elpa_trans_ev_tridi_to_band_host")
+    return Q
+
+
+def workspace_bytes(n, nbw, opts=None):
+    o, op = _opts_ptr(opts)
+    return int(_lib.elpa_b200_workspace_bytes(int(n), int(nbw), op))
+
+
+def prepare(n, nbw, hh_v, hh_tau, workspace, stream=None, opts=None):
+    """Prepare the reflectors into `workspace` (a CUDA uint8 tensor of workspace_bytes())."""
+    o, op = _opts_ptr(opts)
+    s = _stream_handle(stream, hh_v.device)
+    wptr = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None and workspace.numel() else None
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    rc = _lib.elpa_b200_prepare(int(n), int(nbw), _dev_ptr(hh_v, "hh_v"), _dev_ptr(hh_tau, "hh_tau"),
+                                wptr, nbytes, s, op)
+    _check(rc, "elpa_b200_prepare")
+
+
+def apply_prepared(n, nbw, workspace, Q, hh_v=None, hh_tau=None, stream=None, opts=None):
+    nev, ldq = _q_ldq(Q)
+    o, op = _opts_ptr(opts)
+    s = _stream_handle(stream, Q.device)
+    wptr = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None and workspace.numel() else None
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    rc = _lib.elpa_b200_apply_prepared(int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v"),
+                                       _dev_ptr(hh_tau, "hh_tau"), wptr, nbytes, _dev_ptr(Q, "Q"),
+                                       int(ldq), s, op)
+    _check(rc, "elpa_b200_apply_prepared")
+    return Q
+
+
+def describe(n, nbw, nev, opts=None):
+    """(number of kernel launches per call, launch description string)."""
+    o, op = _opts_ptr(opts)
+    buf = ctypes.create_string_buffer(256)
+    rc = _lib.elpa_b200_describe(int(n), int(nbw), int(nev), op, buf, 256)
+    if rc < 0:
+        raise ElpaB200Error(rc, "elpa_b200_describe")
+    return rc, buf.value.decode()
+
+
+def credited_flops(n, nbw, nev):
+    """North-star flop credit: 4 * nbw * nev per reflector (BASELINE.json metric)."""
+    return 4.0 * nbw * nev * hh_count(n, nbw)

@@ -1,0 +1,323 @@
+// elpa_b200.cu — C-ABI host library (include/elpa_b200.h): validation, closed-form
+// reflector geometry, workspace handling and launch configuration for the sm_100a kernels.
+// Build: see paper_1811_01277_b200/build.py (nvcc -gencode arch=compute_100a,code=sm_100a).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/elpa_b200.h"
+#include "geometry.cuh"
+#include "kernel_dmma.cuh"
+#include "kernel_prep.cuh"
+#include "kernel_reference.cuh"
+
+using namespace elpa_b200;
+
+namespace {
+
+constexpr int kMaxSms = 148;
+
+struct Plan {
+    int kernel = ELPA_B200_KERNEL_REFERENCE;
+    int b8 = 0, D = 1, CW = 1, NCT = 1;
+    int tiles_per_cta = 1;
+    int64_t grid = 1;
+    int threads = 128;
+    size_t smem = 0;
+    int64_t ws_bytes = 0;
+};
+
+int sm_count() {
+    int dev = 0, n = kMaxSms;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : kMaxSms;
+}
+
+bool b8_supported(int64_t nbw) {
+    if (nbw % 8) return false;
+    const int64_t b8 = nbw / 8;
+    return b8 == 1 || b8 == 2 || b8 == 4 || b8 == 8;
+}
+
+// (D, CW, NCT) menu of compiled DMMA configurations
+struct Shape { int D, CW, NCT; };
+constexpr Shape kShapes[] = {
+    {1, 10, 2}, {2, 4, 2}, {4, 2, 2}, {8, 1, 2}, {4, 4, 1}, {8, 2, 1}, {2, 8, 1}, {1, 16, 1},
+};
+
+bool shape_compiled(int D, int CW, int NCT) {
+    for (const Shape &s : kShapes)
+        if (s.D == D && s.CW == CW && s.NCT == NCT) return true;
+    return false;
+}
+
+size_t dmma_smem(int b8, int D, int CW, int NCT) {
+    const size_t blob = size_t(128) * (b8 + 1) + 64;
+    return size_t(2) * D * blob * 8 + size_t(2) * D * CW * NCT * 64 * 8 + 64;
+}
+
+// Automatic choice: balance 8-column tiles over the SMs (one CTA per SM, persistent over
+// all depths); when there are few tiles per SM, pipeline more depths per CTA so each SM
+// keeps >= ~16 (depth, tile) DMMA streams in flight.
+void auto_shape(int64_t ntile, int b8, int &D, int &CW, int &NCT) {
+    const int sms = sm_count();
+    const double per_sm = double(ntile) / sms;
+    if (per_sm > 10) { D = 1; CW = 10; NCT = 2; }
+    else if (per_sm > 5) { D = 2; CW = 4; NCT = 2; }
+    else if (per_sm > 2.5) { D = 4; CW = 2; NCT = 2; }
+    else { D = 8; CW = 1; NCT = 2; }
+    (void)b8;
+}
+
+int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
+    int kernel = o ? o->kernel : ELPA_B200_KERNEL_AUTO;
+    if (kernel < ELPA_B200_KERNEL_AUTO || kernel > ELPA_B200_KERNEL_DMMA) return ELPA_B200_ERR_ARG;
+    if (kernel == ELPA_B200_KERNEL_AUTO)
+        kernel = b8_supported(nbw) ? ELPA_B200_KERNEL_DMMA : ELPA_B200_KERNEL_REFERENCE;
+    if (kernel == ELPA_B200_KERNEL_DMMA && !b8_supported(nbw)) return ELPA_B200_ERR_ARG;
+    p.kernel = kernel;
+    if (kernel == ELPA_B200_KERNEL_REFERENCE) {
+        p.threads = 128;
+        p.grid = (nev + 127) / 128;
+        p.ws_bytes = 0;
+        return ELPA_B200_OK;
+    }
+    p.b8 = int(nbw / 8);
+    const int64_t ntile = (nev + 7) / 8;
+    int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NCT = o ? o->tiles_per_warp : 0;
+    if (D == 0 && CW == 0 && NCT == 0) auto_shape(ntile, p.b8, D, CW, NCT);
+    if (!shape_compiled(D, CW, NCT)) return ELPA_B200_ERR_ARG;
+    p.D = D; p.CW = CW; p.NCT = NCT;
+    const int cap = CW * NCT;
+    int tpc = o ? o->tiles_per_cta : 0;
+    if (tpc == 0) {
+        const int sms = sm_count();
+        int64_t t = (ntile + sms - 1) / sms;
+        tpc = int(t < 1 ? 1 : (t > cap ? cap : t));
+    }
+    if (tpc < 1 || tpc > cap) return ELPA_B200_ERR_ARG;
+    p.tiles_per_cta = tpc;
+    p.grid = ntile > 0 ? (ntile + tpc - 1) / tpc : 0;
+    p.threads = 32 * D * CW;
+    p.smem = dmma_smem(p.b8, D, CW, NCT);
+    const int64_t M = num_depths(n, nbw);
+    p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1) * 8 : 0;
+    return ELPA_B200_OK;
+}
+
+int check_device() {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return ELPA_B200_ERR_DEVICE;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+        return ELPA_B200_ERR_DEVICE;
+    return (major == 10 && minor == 0) ? ELPA_B200_OK : ELPA_B200_ERR_DEVICE;
+}
+
+int validate(int64_t n, int64_t nbw, int64_t nev, const void *hh_v, const void *hh_tau, const void *Q,
+             int64_t ldq, bool check_q_align) {
+    if (n < 0 || nbw < 1 || nev < 0 || nev > n || ldq < (n > 1 ? n : 1)) return ELPA_B200_ERR_ARG;
+    const int64_t R = hh_total(n, nbw);
+    if (R > 0 && nev > 0 && (!hh_v || !hh_tau || !Q)) return ELPA_B200_ERR_NULL;
+    if (check_q_align && R > 0 && nev > 0 && ((ldq & 1) || (reinterpret_cast<uintptr_t>(Q) & 15)))
+        return ELPA_B200_ERR_ALIGN;
+    return ELPA_B200_OK;
+}
+
+template <int B8>
+int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws, cudaStream_t s) {
+    const int64_t M = num_depths(n, 8 * B8);
+    const int64_t G0 = groups_at_depth(n, B8, 0);
+    dim3 grid(unsigned((G0 + 3) / 4), unsigned(M));
+    prep_dmma_kernel<B8><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
+    return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+}
+
+template <int B8, int D, int CW, int NCT>
+int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
+                      cudaStream_t s) {
+    auto kern = apply_dmma_kernel<B8, D, CW, NCT>;
+    const size_t smem = DmmaCfg<B8, D, CW, NCT>::SMEM;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        return ELPA_B200_ERR_CUDA;
+    kern<<<unsigned(p.grid), DmmaCfg<B8, D, CW, NCT>::THREADS, smem, s>>>(n, nev, ws, Q, ldq, p.tiles_per_cta);
+    return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+}
+
+template <int B8>
+int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
+                   cudaStream_t s) {
+#define ELPA_SHAPE(D_, CW_, NCT_) \
+    if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_) return launch_dmma_shape<B8, D_, CW_, NCT_>(p, n, nev, ws, Q, ldq, s);
+    ELPA_SHAPE(1, 10, 2)
+    ELPA_SHAPE(2, 4, 2)
+    ELPA_SHAPE(4, 2, 2)
+    ELPA_SHAPE(8, 1, 2)
+    ELPA_SHAPE(4, 4, 1)
+    ELPA_SHAPE(8, 2, 1)
+    ELPA_SHAPE(2, 8, 1)
+    ELPA_SHAPE(1, 16, 1)
+#undef ELPA_SHAPE
+    return ELPA_B200_ERR_ARG;
+}
+
+int prepare_impl(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, void *ws, cudaStream_t s) {
+    if (p.kernel != ELPA_B200_KERNEL_DMMA || p.ws_bytes == 0) return ELPA_B200_OK;
+    double *w = static_cast<double *>(ws);
+    switch (p.b8) {
+        case 1: return launch_prep<1>(n, hh_v, hh_tau, w, s);
+        case 2: return launch_prep<2>(n, hh_v, hh_tau, w, s);
+        case 4: return launch_prep<4>(n, hh_v, hh_tau, w, s);
+        case 8: return launch_prep<8>(n, hh_v, hh_tau, w, s);
+    }
+    return ELPA_B200_ERR_ARG;
+}
+
+int apply_impl(const Plan &p, int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+               const void *ws, double *Q, int64_t ldq, cudaStream_t s) {
+    if (p.kernel == ELPA_B200_KERNEL_REFERENCE) {
+        apply_reference_kernel<<<unsigned(p.grid), p.threads, 0, s>>>(n, nbw, nev, hh_v, hh_tau, Q, ldq);
+        return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+    }
+    const double *w = static_cast<const double *>(ws);
+    switch (p.b8) {
+        case 1: return launch_dmma_b8<1>(p, n, nev, w, Q, ldq, s);
+        case 2: return launch_dmma_b8<2>(p, n, nev, w, Q, ldq, s);
+        case 4: return launch_dmma_b8<4>(p, n, nev, w, Q, ldq, s);
+        case 8: return launch_dmma_b8<8>(p, n, nev, w, Q, ldq, s);
+    }
+    return ELPA_B200_ERR_ARG;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t elpa_hh_count(int64_t n, int64_t nbw) {
+    if (n < 0 || nbw < 1) return -1;
+    return hh_total(n, nbw);
+}
+
+const char *elpa_b200_strerror(int code) {
+    switch (code) {
+        case ELPA_B200_OK: return "ok";
+        case ELPA_B200_ERR_ARG: return "invalid argument (n, nbw, nev, ldq or options)";
+        case ELPA_B200_ERR_NULL: return "required pointer is NULL";
+        case ELPA_B200_ERR_ALIGN: return "misaligned Q (ldq must be even, Q 16-byte aligned) or workspace";
+        case ELPA_B200_ERR_DEVICE: return "current device is not an sm_100 (B200) GPU";
+        case ELPA_B200_ERR_CUDA: return "CUDA runtime error or kernel launch failure";
+        case ELPA_B200_ERR_SPACE: return "workspace too small";
+    }
+    return "unknown error code";
+}
+
+int64_t elpa_b200_workspace_bytes(int64_t n, int64_t nbw, const elpa_b200_opts *opts) {
+    if (n < 0 || nbw < 1) return -1;
+    Plan p;
+    if (make_plan(n, nbw, n > 0 ? n : 1, opts, p) != ELPA_B200_OK) return -1;
+    return p.ws_bytes;
+}
+
+int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *opts, char *buf, size_t buflen) {
+    if (n < 0 || nbw < 1 || nev < 0 || nev > n) return ELPA_B200_ERR_ARG;
+    Plan p;
+    int rc = make_plan(n, nbw, nev, opts, p);
+    if (rc != ELPA_B200_OK) return rc;
+    if (buf && buflen)
+        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NCT=%d tiles_per_cta=%d grid=%lld block=%d smem=%zu ws=%lld",
+                 p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : "reference", p.b8, p.D, p.CW, p.NCT, p.tiles_per_cta,
+                 (long long)p.grid, p.threads, p.smem, (long long)p.ws_bytes);
+    if (hh_total(n, nbw) == 0 || nev == 0) return 0;
+    return p.kernel == ELPA_B200_KERNEL_DMMA ? 2 : 1;
+}
+
+int elpa_b200_prepare(int64_t n, int64_t nbw, const double *hh_v, const double *hh_tau, void *workspace,
+                      size_t workspace_bytes, elpa_b200_stream_t stream, const elpa_b200_opts *opts) {
+    if (n < 0 || nbw < 1) return ELPA_B200_ERR_ARG;
+    Plan p;
+    int rc = make_plan(n, nbw, n > 0 ? n : 1, opts, p);
+    if (rc != ELPA_B200_OK) return rc;
+    if (hh_total(n, nbw) == 0 || p.ws_bytes == 0) return ELPA_B200_OK;
+    if (!hh_v || !hh_tau || !workspace) return ELPA_B200_ERR_NULL;
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return ELPA_B200_ERR_ALIGN;
+    if (workspace_bytes < size_t(p.ws_bytes)) return ELPA_B200_ERR_SPACE;
+    if ((rc = check_device()) != ELPA_B200_OK) return rc;
+    return prepare_impl(p, n, hh_v, hh_tau, workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+                             const void *workspace, size_t workspace_bytes, double *Q, int64_t ldq,
+                             elpa_b200_stream_t stream, const elpa_b200_opts *opts) {
+    Plan p;
+    int rc = validate(n, nbw, nev, (opts && opts->kernel == ELPA_B200_KERNEL_REFERENCE) ? hh_v : (const void *)1,
+                      (opts && opts->kernel == ELPA_B200_KERNEL_REFERENCE) ? hh_tau : (const void *)1, Q, ldq, true);
+    if (rc != ELPA_B200_OK) return rc;
+    if ((rc = make_plan(n, nbw, nev, opts, p)) != ELPA_B200_OK) return rc;
+    if (hh_total(n, nbw) == 0 || nev == 0) return ELPA_B200_OK;
+    if (p.kernel == ELPA_B200_KERNEL_REFERENCE && (!hh_v || !hh_tau)) return ELPA_B200_ERR_NULL;
+    if (p.kernel == ELPA_B200_KERNEL_DMMA) {
+        if (!workspace) return ELPA_B200_ERR_NULL;
+        if (reinterpret_cast<uintptr_t>(workspace) & 255) return ELPA_B200_ERR_ALIGN;
+        if (workspace_bytes < size_t(p.ws_bytes)) return ELPA_B200_ERR_SPACE;
+    }
+    if ((rc = check_device()) != ELPA_B200_OK) return rc;
+    return apply_impl(p, n, nbw, nev, hh_v, hh_tau, workspace, Q, ldq, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int elpa_trans_ev_tridi_to_band_ex(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+                                   double *Q, int64_t ldq, elpa_b200_stream_t stream, const elpa_b200_opts *opts) {
+    int rc = validate(n, nbw, nev, hh_v, hh_tau, Q, ldq, true);
+    if (rc != ELPA_B200_OK) return rc;
+    Plan p;
+    if ((rc = make_plan(n, nbw, nev, opts, p)) != ELPA_B200_OK) return rc;
+    if (hh_total(n, nbw) == 0 || nev == 0) return ELPA_B200_OK;
+    if ((rc = check_device()) != ELPA_B200_OK) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    void *ws = nullptr;
+    if (p.ws_bytes > 0 && cudaMallocAsync(&ws, size_t(p.ws_bytes), s) != cudaSuccess) return ELPA_B200_ERR_CUDA;
+    rc = prepare_impl(p, n, hh_v, hh_tau, ws, s);
+    if (rc == ELPA_B200_OK) rc = apply_impl(p, n, nbw, nev, hh_v, hh_tau, ws, Q, ldq, s);
+    if (ws && cudaFreeAsync(ws, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    return rc;
+}
+
+int elpa_trans_ev_tridi_to_band(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+                                double *Q, int64_t ldq, elpa_b200_stream_t stream) {
+    return elpa_trans_ev_tridi_to_band_ex(n, nbw, nev, hh_v, hh_tau, Q, ldq, stream, nullptr);
+}
+
+int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+                                     double *Q, int64_t ldq, elpa_b200_stream_t stream, const elpa_b200_opts *opts) {
+    int rc = validate(n, nbw, nev, hh_v, hh_tau, Q, ldq, false);
+    if (rc != ELPA_B200_OK) return rc;
+    if (ldq & 1) return ELPA_B200_ERR_ALIGN;
+    Plan p;
+    if ((rc = make_plan(n, nbw, nev, opts, p)) != ELPA_B200_OK) return rc;
+    const int64_t R = hh_total(n, nbw);
+    if (R == 0 || nev == 0) return ELPA_B200_OK;
+    if ((rc = check_device()) != ELPA_B200_OK) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t bq = size_t(ldq) * nev * 8, bv = size_t(R) * nbw * 8, bt = size_t(R) * 8;
+    char *buf = nullptr;
+    const size_t off_v = (bq + 255) & ~size_t(255), off_t = off_v + ((bv + 255) & ~size_t(255));
+    const size_t off_w = off_t + ((bt + 255) & ~size_t(255));
+    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), off_w + size_t(p.ws_bytes), s) != cudaSuccess)
+        return ELPA_B200_ERR_CUDA;
+    double *dQ = reinterpret_cast<double *>(buf), *dv = reinterpret_cast<double *>(buf + off_v);
+    double *dt = reinterpret_cast<double *>(buf + off_t);
+    void *ws = p.ws_bytes ? buf + off_w : nullptr;
+    if (cudaMemcpyAsync(dv, hh_v, bv, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(dt, hh_tau, bt, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(dQ, Q, bq, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        rc = ELPA_B200_ERR_CUDA;
+    if (rc == ELPA_B200_OK) rc = prepare_impl(p, n, dv, dt, ws, s);
+    if (rc == ELPA_B200_OK) rc = apply_impl(p, n, nbw, nev, dv, dt, ws, dQ, ldq, s);
+    if (rc == ELPA_B200_OK && cudaMemcpyAsync(Q, dQ, bq, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        rc = ELPA_B200_ERR_CUDA;
+    if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    return rc;
+}
+
+}  // extern "C"

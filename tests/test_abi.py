@@ -1,0 +1,106 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every symbol the
+header declares, counts reflectors by the closed form, and rejects bad arguments before
+touching the device (DESIGN.md §4 validation table)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1811_01277_b200 as eb
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "elpa_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(elpa_\w+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    names = header_functions()
+    assert len(names) >= 9
+    lib = ctypes.CDLL(eb.LIBRARY_PATH)
+    for nm in names:
+        assert hasattr(lib, nm), nm
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", eb.LIBRARY_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+@pytest.mark.parametrize("n,b", [(0, 4), (1, 4), (2, 4), (3, 2), (4, 3), (50, 1), (100, 16),
+                                 (512, 16), (4096, 32), (20000, 64), (60000, 64), (97, 200)])
+def test_hh_count_matches_oracle_enumeration(n, b):
+    if n <= 20000:
+        assert eb.hh_count(n, b) == oracle.count(n, b)
+    want = {(20000, 64): 3134382, (60000, 64): 28153132, (4096, 32): 263936, (512, 16): 8384}
+    if (n, b) in want:
+        assert eb.hh_count(n, b) == want[(n, b)]
+
+
+def test_hh_count_bad_args():
+    assert eb.hh_count(-1, 4) == -1
+    assert eb.hh_count(10, 0) == -1
+
+
+def test_strerror():
+    for c in (eb.OK, eb.ERR_ARG, eb.ERR_NULL, eb.ERR_ALIGN, eb.ERR_DEVICE, eb.ERR_CUDA, eb.ERR_SPACE):
+        assert eb.strerror(c) and eb.strerror(c) != "unknown error code"
+    assert eb.strerror(42) == "unknown error code"
+
+
+def _call(n, nbw, nev, hv, ht, q, ldq, opts=None):
+    lib = eb._lib
+    if opts is None:
+        return lib.elpa_trans_ev_tridi_to_band(n, nbw, nev, hv, ht, q, ldq, None)
+    return lib.elpa_trans_ev_tridi_to_band_ex(n, nbw, nev, hv, ht, q, ldq, None, ctypes.byref(eb.Opts(**opts)))
+
+
+FAKE = ctypes.c_void_p(0x10000)      # never dereferenced: validation fails first
+
+
+def test_validation_order_before_device():
+    assert _call(-1, 4, 1, FAKE, FAKE, FAKE, 10) == eb.ERR_ARG          # n < 0
+    assert _call(10, 0, 1, FAKE, FAKE, FAKE, 10) == eb.ERR_ARG          # nbw < 1
+    assert _call(10, 4, -1, FAKE, FAKE, FAKE, 10) == eb.ERR_ARG         # nev < 0
+    assert _call(10, 4, 11, FAKE, FAKE, FAKE, 10) == eb.ERR_ARG         # nev > n
+    assert _call(10, 4, 5, FAKE, FAKE, FAKE, 9) == eb.ERR_ARG           # ldq < n
+    assert _call(10, 4, 5, None, FAKE, FAKE, 10) == eb.ERR_NULL
+    assert _call(10, 4, 5, FAKE, None, FAKE, 10) == eb.ERR_NULL
+    assert _call(10, 4, 5, FAKE, FAKE, None, 10) == eb.ERR_NULL
+    assert _call(11, 4, 5, FAKE, FAKE, FAKE, 11) == eb.ERR_ALIGN        # ldq odd
+    assert _call(10, 4, 5, FAKE, FAKE, ctypes.c_void_p(0x10008), 10) == eb.ERR_ALIGN
+    assert _call(10, 8, 5, FAKE, FAKE, FAKE, 10, dict(kernel=2, depth_warps=3, col_warps=1, tiles_per_warp=1)) == eb.ERR_ARG
+    assert _call(10, 6, 5, FAKE, FAKE, FAKE, 10, dict(kernel=2)) == eb.ERR_ARG   # DMMA needs nbw % 8 == 0
+    assert _call(10, 8, 5, FAKE, FAKE, FAKE, 10, dict(kernel=7)) == eb.ERR_ARG
+
+
+def test_trivial_calls_touch_nothing():
+    # R == 0 (n < 3, nbw == 1) or nev == 0: OK with no memory access, even with NULLs
+    assert _call(2, 4, 2, None, None, None, 2) == eb.OK
+    assert _call(50, 1, 5, None, None, None, 50) == eb.OK
+    assert _call(50, 8, 0, None, None, None, 50) == eb.OK
+    assert _call(0, 8, 0, None, None, None, 1) == eb.OK
+
+
+def test_describe_and_workspace():
+    k, desc = eb.describe(20000, 64, 20000)
+    assert k == 2 and "kernel=dmma" in desc and "b8=8" in desc
+    k, desc = eb.describe(100, 6, 10)
+    assert k == 1 and "kernel=reference" in desc
+    assert eb.describe(2, 4, 2)[0] == 0
+    # workspace = groups * (128*lambda + 64) doubles
+    n, b = 4096, 32
+    b8, lam = b // 8, b // 8 + 1
+    M = (n - 3) // b + 1
+    G0 = ((n - 2) >> 3) + 1
+    groups = sum(G0 - m * b8 for m in range(M))
+    assert eb.workspace_bytes(n, b) == groups * (128 * lam + 64) * 8
+    assert eb.workspace_bytes(100, 6) == 0

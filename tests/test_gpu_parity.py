@@ -1,0 +1,173 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded
+inputs.  Bar (BASELINE.json north_star): max|dQ| / max|Q_oracle| <= 1e-12 and eigen-residual
+<= 1e-13; the REFERENCE kernel must be bitwise equal to the oracle (R10)."""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import band_matrix, synthetic_reflectors, synthetic_q_np, config_seed
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def eb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    import paper_1811_01277_b200 as m
+    return m
+
+
+def _rel(got, want):
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
+
+
+def run_gpu(eb, n, nbw, hh_v, hh_tau, Q, opts=None):
+    import torch
+    dv = torch.from_numpy(np.ascontiguousarray(hh_v)).cuda()
+    dt = torch.from_numpy(np.ascontiguousarray(hh_tau)).cuda()
+    dq = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
+    eb.trans_ev_tridi_to_band(n, nbw, dv, dt, dq, opts=opts)
+    torch.cuda.synchronize()
+    return dq.cpu().numpy()
+
+
+def synth_case(n, nbw, nev, seed, ldq=None):
+    s, L = oracle.schedule(n, nbw)
+    hv, tau = synthetic_reflectors(len(s), nbw, seed)
+    Q = synthetic_q_np(n, 0, nev, seed, ldq=ldq)
+    return hv, tau, s, L, Q
+
+
+# ------------------------------------------------------------------ reference kernel: bitwise
+@pytest.mark.parametrize("n,nbw,nev", [(512, 16, 64), (37, 5, 9), (100, 7, 33), (64, 63, 10), (3, 2, 3)])
+def test_reference_kernel_bitwise(eb, n, nbw, nev):
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 5 + n)
+    want = oracle.apply(hv, tau, s, L, Q)
+    got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_REFERENCE))
+    assert np.array_equal(got, want)
+
+
+def test_reference_kernel_bitwise_real_C1(eb):
+    case = oracle.make_case(512, 16, 512, config_seed(1))
+    got = run_gpu(eb, 512, 16, case["hh_v"], case["hh_tau"], case["Qin"], opts=dict(kernel=eb.KERNEL_REFERENCE))
+    assert np.array_equal(got, case["Qref"])
+
+
+# ------------------------------------------------------------------ DMMA kernel: tolerance
+SHAPES = [(1, 10, 2), (2, 4, 2), (4, 2, 2), (8, 1, 2), (4, 4, 1), (8, 2, 1), (2, 8, 1), (1, 16, 1)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("nbw", [8, 16, 32, 64])
+def test_dmma_all_shapes(eb, shape, nbw):
+    D, CW, NCT = shape
+    n, nev = 301, 45                          # ragged: n odd, nev not a multiple of 8
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, nbw * 13 + D, ldq=302)
+    want = oracle.apply(hv, tau, s, L, Q)
+    for tpc in sorted({1, CW * NCT, max(1, CW * NCT - 1)}):
+        got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
+                                                         tiles_per_warp=NCT, tiles_per_cta=tpc))
+        assert _rel(got[:, :n], want[:, :n]) <= TOL, (shape, tpc)
+        assert np.array_equal(got[:, n:], Q[:, n:])      # ldq padding untouched
+
+
+@pytest.mark.parametrize("n,nbw,nev", [(3, 8, 3), (4, 8, 4), (5, 8, 5), (10, 8, 10), (11, 8, 1), (17, 16, 17),
+                                       (66, 64, 66), (67, 64, 13), (130, 64, 130), (1000, 32, 100),
+                                       (2049, 64, 77)])
+def test_dmma_edge_sizes(eb, n, nbw, nev):
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 77 + n, ldq=n + (n & 1))
+    want = oracle.apply(hv, tau, s, L, Q)
+    got = run_gpu(eb, n, nbw, hv, tau, Q)
+    assert _rel(got, want) <= TOL
+
+
+def test_dmma_tau_zero_and_v0_ignored(eb):
+    n, nbw, nev = 200, 16, 24
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 3)
+    tau = tau.copy()
+    tau[::3] = 0.0
+    hv2 = hv.copy()
+    hv2[:, 0] = 123.0                         # element 0 must be treated as 1 (ELPA keeps tau there)
+    for i, Lr in enumerate(L):
+        hv2[i, Lr:] = np.nan                  # elements >= L must never be read
+    want = oracle.apply(hv, tau, s, L, Q)
+    got = run_gpu(eb, n, nbw, hv2, tau, Q)
+    assert _rel(got, want) <= TOL
+    got = run_gpu(eb, n, nbw, hv, np.zeros_like(tau), Q)
+    assert np.array_equal(got, Q)
+
+
+def test_dmma_real_C1_and_residual(eb):
+    case = oracle.make_case(512, 16, 512, config_seed(1))
+    got = run_gpu(eb, 512, 16, case["hh_v"], case["hh_tau"], case["Qin"])
+    assert _rel(got, case["Qref"]) <= TOL
+    assert oracle.residual(case["band"], got, case["lam"]) <= 1e-13
+
+
+def test_dmma_real_C2_residual(eb):
+    case = oracle.make_case(4096, 32, 4096, config_seed(2))
+    got = run_gpu(eb, 4096, 32, case["hh_v"], case["hh_tau"], case["Qin"])
+    assert _rel(got, case["Qref"]) <= TOL
+    assert oracle.residual(case["band"], got, case["lam"]) <= 1e-13
+
+
+def test_column_independence_bitwise(eb):
+    """Sharding invariant (§8e): any column range computed alone is bitwise equal to the
+    same columns of the full call, whatever its tile/CTA placement."""
+    n, nbw, nev = 700, 32, 160
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 12, ldq=700)
+    full = run_gpu(eb, n, nbw, hv, tau, Q)
+    for c0, c1 in [(0, 8), (3, 50), (77, 160), (159, 160)]:
+        part = run_gpu(eb, n, nbw, hv, tau, Q[c0:c1].copy())
+        assert np.array_equal(part, full[c0:c1]), (c0, c1)
+    alt = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=2, depth_warps=8, col_warps=1, tiles_per_warp=2))
+    assert np.array_equal(alt, full)
+
+
+def test_prepare_apply_two_phase(eb):
+    import torch
+    n, nbw, nev = 500, 64, 40
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 99)
+    want = oracle.apply(hv, tau, s, L, Q)
+    dv, dt = torch.from_numpy(hv).cuda(), torch.from_numpy(tau).cuda()
+    ws = torch.empty(eb.workspace_bytes(n, nbw), dtype=torch.uint8, device="cuda")
+    eb.prepare(n, nbw, dv, dt, ws)
+    for half in (slice(0, 20), slice(20, 40)):
+        dq = torch.from_numpy(Q[half].copy()).cuda()
+        eb.apply_prepared(n, nbw, ws, dq)
+        torch.cuda.synchronize()
+        assert _rel(dq.cpu().numpy(), want[half]) <= TOL
+
+
+def test_host_entry_point(eb):
+    import torch
+    n, nbw, nev = 900, 64, 50
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 4)
+    want = oracle.apply(hv, tau, s, L, Q)
+    hq = torch.from_numpy(Q.copy()).pin_memory()
+    eb.trans_ev_tridi_to_band_host(n, nbw, torch.from_numpy(hv).pin_memory(), torch.from_numpy(tau).pin_memory(), hq)
+    assert _rel(hq.numpy(), want) <= TOL
+
+
+def test_full_size_C3_sampled_columns(eb):
+    """C3 (n = 20000, nbw = 64, nev = 20000) in the launch configuration bench.py times:
+    the oracle recomputes 12 sampled columns (column independence makes them exact)."""
+    import torch
+    from inputs import synthetic_q_torch
+    n, nbw, nev = 20000, 64, 20000
+    seed = config_seed(3)
+    R = eb.hh_count(n, nbw)
+    hv, tau = synthetic_reflectors(R, nbw, seed)
+    dq = synthetic_q_torch(n, 0, nev, seed, device="cuda")
+    eb.trans_ev_tridi_to_band(n, nbw, torch.from_numpy(hv).cuda(), torch.from_numpy(tau).cuda(), dq)
+    torch.cuda.synchronize()
+    cols = [0, 1, 7, 8, 4999, 10000, 12345, 15000, 19991, 19992, 19998, 19999]
+    got = dq[cols].cpu().numpy()
+    s, L = oracle.schedule(n, nbw)
+    Qs = np.concatenate([synthetic_q_np(n, c, c + 1, seed) for c in cols])
+    want = oracle.apply(hv, tau, s, L, Qs)
+    assert _rel(got, want) <= TOL
