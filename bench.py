@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""bench.py — FP64 TFLOP/s of trans_ev_tridi_to_band on 1..N B200 (BASELINE.json metric).
+
+One step = one pass of the whole hot path over one synthetic
+problem: [N>1: NCCL broadcast of the reflector set from rank 0] + reflector preparation
+(prep kernel) + application to this rank's nev/N eigenvector columns (apply kernel), inputs
+resident in HBM.  Flops credited 4*nbw*nev per reflector (north_star).  Default workload:
+C3 (n = 20000, nbw = 64, nev = 20000), the north-star target configuration.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the deliberately slow
+plain C program in oracle/) on a bounded column sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from inputs import CONFIGS, config_seed, synthetic_reflectors, synthetic_q_np, synthetic_q_torch  # noqa: E402
+
+METRIC = "trans_ev_tridi_to_band FP64 TFLOP/s (2*n^2*nev) and % roofline, 1/2/4/8 B200"
+UNIT = "TFLOP/s"
+CFG_INDEX = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
+PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.jsonl")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def fp64_peak():
+    """Measured FP64 peaks on this pool's B200 (tools/fp64_peak.cu, profiles/)."""
+    peaks = {"dmma": None, "dfma": None}
+    try:
+        for line in open(PEAKS_FILE):
+            r = json.loads(line)
+            if r.get("test") == "dmma_m8n8k4":
+                peaks["dmma"] = max(peaks["dmma"] or 0, r["tflops"])
+            if r.get("test") == "dfma":
+                peaks["dfma"] = max(peaks["dfma"] or 0, r["tflops"])
+    except OSError:
+        pass
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_rate(n, nbw, nev, seed, ncols, threads=None):
+    """Time the plain CPU oracle (oracle/, never tuned) on `ncols` sampled columns."""
+    import numpy as np
+    import oracle
+    s, L = oracle.schedule(n, nbw)
+    hv, tau = synthetic_reflectors(len(s), nbw, seed)
+    cols = np.linspace(0, nev - 1, ncols).astype(int)
+    Qs = np.concatenate([synthetic_q_np(n, int(c), int(c) + 1, seed) for c in cols])
+    threads = threads or os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.apply(hv, tau, s, L, Qs, nthreads=threads)
+    dt = time.perf_counter() - t0
+    flops = 4.0 * nbw * ncols * len(s)
+    return flops / dt / 1e12, dt, threads, ncols
+
+
+def reference_arm(args):
+    """--impl reference: the CPU oracle on the box's host cores, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n, nbw, nev = CONFIGS[args.config]
+    seed = config_seed(CFG_INDEX[args.config])
+    ncols = 16
+    rates, times = [], []
+    for i in range(args.warmup + args.steps):
+        r, dt, thr, nc = cpu_oracle_rate(n, nbw, nev, seed, ncols)
+        if i >= args.warmup:
+            rates.append(r)
+            times.append(dt)
+    value = statistics.median(rates)
+    ms = statistics.median(times) * 1e3
+    sample = f"{ncols} evenly spaced columns of {args.config} per step ({4.0 * nbw * ncols * (n - 2):.3g}+ flops)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} n={n} nbw={nbw} nev={nev}", "n": n, "nbw": nbw, "nev": nev},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0}))
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1811_01277_b200 as eb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, nbw, nev = CONFIGS[args.config]
+    seed = config_seed(CFG_INDEX[args.config])
+    R = eb.hh_count(n, nbw)
+    c0, c1 = (rank * nev) // world, ((rank + 1) * nev) // world
+    nev_loc = c1 - c0
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs: reflectors generated on rank 0 (host), Q shard generated on-device
+    hh = torch.empty(R * (nbw + 1), dtype=torch.float64, device=dev)   # packed hh_v || hh_tau
+    if rank == 0:
+        hv_np, tau_np = synthetic_reflectors(R, nbw, seed)
+        hh[:R * nbw].copy_(torch.from_numpy(hv_np).reshape(-1))
+        hh[R * nbw:].copy_(torch.from_numpy(tau_np))
+    hh_v, hh_tau = hh[:R * nbw].view(R, nbw), hh[R * nbw:]
+    Q = synthetic_q_torch(n, c0, c1, seed, device=dev)
+    ws = torch.empty(eb.workspace_bytes(n, nbw), dtype=torch.uint8, device=dev)
+    nlaunch, desc = eb.describe(n, nbw, nev_loc)
+    torch.cuda.synchronize()
+
+    ev_apply = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
+
+    def step(i=None):
+        if world > 1:
+            dist.broadcast(hh, src=0)
+        eb.prepare(n, nbw, hh_v, hh_tau, ws, stream=stream)
+        if i is not None:
+            ev_apply[i][0].record(stream)
+        eb.apply_prepared(n, nbw, ws, Q, stream=stream)
+        if i is not None:
+            ev_apply[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_local = t0.elapsed_time(t1)
+    apply_ms = [a.elapsed_time(b) for a, b in ev_apply]
+    ms = ms_local
+    if world > 1:
+        tt = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    flops_total = 4.0 * nbw * nev * R                    # all ranks together (credited)
+    value = flops_total / (ms_per_step * 1e-3) / 1e12
+
+    # ---- sampled parity at full size (rank 0): oracle recomputes a few columns of this run
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        import oracle
+        total_apps = args.warmup + args.steps
+        cols = [0, nev_loc // 2, nev_loc - 1]
+        s_arr, L_arr = oracle.schedule(n, nbw)
+        hv_np2, tau_np2 = synthetic_reflectors(R, nbw, seed)
+        Qs = np.concatenate([synthetic_q_np(n, c0 + c, c0 + c + 1, seed) for c in cols])
+        for _ in range(total_apps):
+            Qs = oracle.apply(hv_np2, tau_np2, s_arr, L_arr, Qs)
+        got = Q[cols].cpu().numpy()
+        parity = float(np.abs(got - Qs).max() / np.abs(Qs).max())
+
+    # ---- end to end through the host-buffer C-ABI entry point (pinned host memory)
+    e2e = None
+    if not args.no_e2e:
+        hvh = hh_v.cpu().pin_memory()
+        tauh = hh_tau.cpu().pin_memory()
+        Qh = Q.cpu().pin_memory()
+        eb.trans_ev_tridi_to_band_host(n, nbw, hvh, tauh, Qh, stream=stream)      # warm the pool
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k_e2e = max(1, min(args.steps, 3))
+        e0.record(stream)
+        for _ in range(k_e2e):
+            eb.trans_ev_tridi_to_band_host(n, nbw, hvh, tauh, Qh, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / k_e2e
+        if world > 1:
+            tt = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt.item())
+        e2e = {"value": flops_total / (e_ms * 1e-3) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int((R * nbw + R) * 8 + nev_loc * n * 8),
+               "d2h_bytes_per_step": int(nev_loc * n * 8), "ms_per_step": e_ms, "steps": k_e2e,
+               "path": "elpa_trans_ev_tridi_to_band_host (per-rank host buffers)"}
+
+    # ---- roofline of the dominant kernel (apply): achieved credited flops / launch time
+    peaks = fp64_peak()
+    peak = peaks["dmma"] or 36.98
+    apply_avg = sum(apply_ms) / len(apply_ms)
+    achieved = 4.0 * nbw * nev_loc * R / (apply_avg * 1e-3) / 1e12
+    traffic = None
+    try:
+        summ = json.load(open(NCU_SUMMARY))
+        key = f"{args.config}:{world}"
+        if key in summ:
+            traffic = summ[key].get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "apply_dmma_kernel",
+                "peak_source": "measured FP64 DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peaks_r01.jsonl)",
+                "apply_ms": apply_avg, "exact_flops_frac": None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r, dt, thr, nc = cpu_oracle_rate(n, nbw, nev, seed, 256)
+        cpu = {"value": r, "unit": UNIT, "cores": thr, "kind": "oracle",
+               "sample": f"{nc} evenly spaced columns of {args.config} (all {R} reflectors), {dt:.1f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} n={n} nbw={nbw} nev={nev}", "n": n, "nbw": nbw, "nev": nev,
+                       "nev_per_gpu": nev_loc, "reflectors": R, "parallelism": f"nev-sharded x{world}",
+                       "l2": "inputs larger than L2 (Q shard %.2f GB, hh_v %.2f GB)" % (nev_loc * n * 8 / 1e9, R * nbw * 8 / 1e9),
+                       "kernel": desc, "step": ("bcast+" if world > 1 else "") + "prepare+apply"},
+            "clocks": clk.summary(), "gpu_launches": nlaunch * args.steps, "roofline": roofline,
+            "cpu_baseline": cpu, "e2e": e2e, "parity_max_rel_err_sampled": parity,
+            "apply_ms_per_launch": apply_avg,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

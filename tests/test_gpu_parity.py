@@ -36,6 +36,7 @@ def run_gpu(eb, n, nbw, hh_v, hh_tau, Q, opts=None):
 
 
 def synth_case(n, nbw, nev, seed, ldq=None):
+    ldq = n + (n & 1) if ldq is None else ldq          # the ABI requires an even ldq
     s, L = oracle.schedule(n, nbw)
     hv, tau = synthetic_reflectors(len(s), nbw, seed)
     Q = synthetic_q_np(n, 0, nev, seed, ldq=ldq)
