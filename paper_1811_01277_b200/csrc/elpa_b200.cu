@@ -21,7 +21,9 @@ constexpr int kMaxSms = 148;
 struct Plan {
     int kernel = ELPA_B200_KERNEL_REFERENCE;
     int b8 = 0, D = 1, CW = 1, NCT = 1;
-    int tiles_per_cta = 1;
+    int grid_req = 0;          // requested grid (0 = co-resident maximum)
+    int64_t items = 0;         // (tile group, depth pass) work items
+    int64_t nx = 0;            // tile groups
     int64_t grid = 1;
     int threads = 128;
     size_t smem = 0;
@@ -42,9 +44,9 @@ bool b8_supported(int64_t nbw) {
 
 // (D, CW, NCT) menu of compiled DMMA configurations
 struct Shape { int D, CW, NCT; };
-constexpr Shape kShapes[] = {
-    {1, 10, 2}, {2, 4, 2}, {4, 2, 2}, {8, 1, 2}, {4, 4, 1}, {8, 2, 1}, {2, 8, 1}, {1, 16, 1},
-};
+#define ELPA_SHAPES(X) X(1, 8, 2) X(2, 4, 2) X(2, 2, 4) X(4, 2, 2) X(4, 2, 4) X(4, 1, 4) X(8, 1, 2) X(8, 1, 4) X(4, 4, 1) X(8, 2, 1)
+#define ELPA_SHAPE_ENTRY(D_, CW_, NCT_) {D_, CW_, NCT_},
+constexpr Shape kShapes[] = {ELPA_SHAPES(ELPA_SHAPE_ENTRY)};
 
 bool shape_compiled(int D, int CW, int NCT) {
     for (const Shape &s : kShapes)
@@ -54,19 +56,20 @@ bool shape_compiled(int D, int CW, int NCT) {
 
 size_t dmma_smem(int b8, int D, int CW, int NCT) {
     const size_t blob = size_t(128) * (b8 + 1) + 64;
-    return size_t(2) * D * blob * 8 + size_t(2) * D * CW * NCT * 64 * 8 + 64;
+    const int stages = (D * blob * 8 * 3 <= 150 * 1024) ? 3 : 2;
+    return size_t(stages) * D * blob * 8 + size_t(2) * D * CW * NCT * 64 * 8 + size_t(2) * CW * NCT * 64 * 8 + 64;
 }
 
-// Automatic choice: balance 8-column tiles over the SMs (one CTA per SM, persistent over
-// all depths); when there are few tiles per SM, pipeline more depths per CTA so each SM
-// keeps >= ~16 (depth, tile) DMMA streams in flight.
-void auto_shape(int64_t ntile, int b8, int &D, int &CW, int &NCT) {
+// Automatic choice: D = 4 pipelined depths per work item (HBM traffic for Q
+// is 1/D of a depth-at-a-time sweep), 8 tiles (64 columns) per item so each prepared
+// fragment block in shared memory serves 8 tiles, 2 warps per SMSP; work items
+// (tile group, depth pass) are spread over all SMs, so balance no longer depends on
+// nev / (8 * #SMs).  Narrow problems use 4-tile items to keep >= ~8 items per SM.
+void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT) {
     const int sms = sm_count();
-    const double per_sm = double(ntile) / sms;
-    if (per_sm > 10) { D = 1; CW = 10; NCT = 2; }
-    else if (per_sm > 5) { D = 2; CW = 4; NCT = 2; }
-    else if (per_sm > 2.5) { D = 4; CW = 2; NCT = 2; }
-    else { D = 8; CW = 1; NCT = 2; }
+    const int64_t np4 = (M + 3) / 4;
+    if (((ntile + 7) / 8) * np4 >= 8 * sms) { D = 4; CW = 2; NCT = 4; }
+    else { D = 4; CW = 1; NCT = 4; }
     (void)b8;
 }
 
@@ -85,23 +88,18 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     }
     p.b8 = int(nbw / 8);
     const int64_t ntile = (nev + 7) / 8;
+    const int64_t M = num_depths(n, nbw);
     int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NCT = o ? o->tiles_per_warp : 0;
-    if (D == 0 && CW == 0 && NCT == 0) auto_shape(ntile, p.b8, D, CW, NCT);
+    if (D == 0 && CW == 0 && NCT == 0) auto_shape(ntile, M, p.b8, D, CW, NCT);
     if (!shape_compiled(D, CW, NCT)) return ELPA_B200_ERR_ARG;
     p.D = D; p.CW = CW; p.NCT = NCT;
-    const int cap = CW * NCT;
-    int tpc = o ? o->tiles_per_cta : 0;
-    if (tpc == 0) {
-        const int sms = sm_count();
-        int64_t t = (ntile + sms - 1) / sms;
-        tpc = int(t < 1 ? 1 : (t > cap ? cap : t));
-    }
-    if (tpc < 1 || tpc > cap) return ELPA_B200_ERR_ARG;
-    p.tiles_per_cta = tpc;
-    p.grid = ntile > 0 ? (ntile + tpc - 1) / tpc : 0;
+    p.grid_req = o ? o->grid_ctas : 0;
+    if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
+    p.nx = (ntile + CW * NCT - 1) / (CW * NCT);
+    p.items = p.nx * ((M + D - 1) / D);
+    p.grid = p.items;          // capped by co-residency at launch
     p.threads = 32 * D * CW;
     p.smem = dmma_smem(p.b8, D, CW, NCT);
-    const int64_t M = num_depths(n, nbw);
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1) * 8 : 0;
     return ELPA_B200_OK;
 }
@@ -134,15 +132,38 @@ int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws,
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
 }
 
+// Co-resident grid of the persistent item kernel (every CTA must be resident at once:
+// items wait on items of lower index held by other CTAs).
+template <int B8, int D, int CW, int NCT>
+int64_t dmma_grid(const Plan &p) {
+    auto kern = apply_dmma_kernel<B8, D, CW, NCT>;
+    const size_t smem = DmmaCfg<B8, D, CW, NCT>::SMEM;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<B8, D, CW, NCT>::THREADS, smem) !=
+            cudaSuccess || per_sm < 1)
+        return -1;
+    int64_t g = int64_t(per_sm) * sm_count();
+    if (p.grid_req > 0 && p.grid_req < g) g = p.grid_req;
+    return g < p.items ? g : p.items;
+}
+
 template <int B8, int D, int CW, int NCT>
 int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
                       cudaStream_t s) {
-    auto kern = apply_dmma_kernel<B8, D, CW, NCT>;
-    const size_t smem = DmmaCfg<B8, D, CW, NCT>::SMEM;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-        return ELPA_B200_ERR_CUDA;
-    kern<<<unsigned(p.grid), DmmaCfg<B8, D, CW, NCT>::THREADS, smem, s>>>(n, nev, ws, Q, ldq, p.tiles_per_cta);
-    return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+    const int64_t grid = dmma_grid<B8, D, CW, NCT>(p);
+    if (grid < 1) return ELPA_B200_ERR_CUDA;
+    uint64_t *prog = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&prog), size_t(p.nx) * 8, s) != cudaSuccess) return ELPA_B200_ERR_CUDA;
+    int rc = ELPA_B200_OK;
+    if (cudaMemsetAsync(prog, 0, size_t(p.nx) * 8, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    if (rc == ELPA_B200_OK) {
+        apply_dmma_kernel<B8, D, CW, NCT><<<unsigned(grid), DmmaCfg<B8, D, CW, NCT>::THREADS,
+                                            DmmaCfg<B8, D, CW, NCT>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
+        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    }
+    if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    return rc;
 }
 
 template <int B8>
@@ -150,14 +171,7 @@ int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, doub
                    cudaStream_t s) {
 #define ELPA_SHAPE(D_, CW_, NCT_) \
     if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_) return launch_dmma_shape<B8, D_, CW_, NCT_>(p, n, nev, ws, Q, ldq, s);
-    ELPA_SHAPE(1, 10, 2)
-    ELPA_SHAPE(2, 4, 2)
-    ELPA_SHAPE(4, 2, 2)
-    ELPA_SHAPE(8, 1, 2)
-    ELPA_SHAPE(4, 4, 1)
-    ELPA_SHAPE(8, 2, 1)
-    ELPA_SHAPE(2, 8, 1)
-    ELPA_SHAPE(1, 16, 1)
+    ELPA_SHAPES(ELPA_SHAPE)
 #undef ELPA_SHAPE
     return ELPA_B200_ERR_ARG;
 }
@@ -225,9 +239,9 @@ int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts
     int rc = make_plan(n, nbw, nev, opts, p);
     if (rc != ELPA_B200_OK) return rc;
     if (buf && buflen)
-        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NCT=%d tiles_per_cta=%d grid=%lld block=%d smem=%zu ws=%lld",
-                 p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : "reference", p.b8, p.D, p.CW, p.NCT, p.tiles_per_cta,
-                 (long long)p.grid, p.threads, p.smem, (long long)p.ws_bytes);
+        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NCT=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
+                 p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : "reference", p.b8, p.D, p.CW, p.NCT, (long long)p.items,
+                 p.grid_req, p.threads, p.smem, (long long)p.ws_bytes);
     if (hh_total(n, nbw) == 0 || nev == 0) return 0;
     return p.kernel == ELPA_B200_KERNEL_DMMA ? 2 : 1;
 }

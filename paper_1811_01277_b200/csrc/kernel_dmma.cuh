@@ -59,6 +59,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// 16-byte cp.async global -> shared with zero fill of the bytes past `src_bytes` (0, 8, 16)
+__device__ __forceinline__ void cp_async16_zfill(void *dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Q chunk I/O: lane owns rows r, r+1 (r = 8*chunk + 2*(lane%4)) of column `col`.
 __device__ __forceinline__ double2 load_pair(const double *Q, int64_t ldq, int64_t n, int64_t col,
                                              bool colok, int64_t r) {
@@ -73,6 +82,12 @@ __device__ __forceinline__ double2 load_pair(const double *Q, int64_t ldq, int64
     }
     return v;
 }
+__device__ __forceinline__ void load_pair_async(double2 *dst, const double *Q, int64_t ldq, int64_t n, int64_t col,
+                                                bool colok, int64_t r) {
+    const bool ok = colok && r >= 0 && r < n;
+    const double *src = ok ? Q + col * ldq + r : Q;
+    cp_async16_zfill(dst, src, ok ? (r + 1 < n ? 16u : 8u) : 0u);
+}
 __device__ __forceinline__ void store_pair(double *Q, int64_t ldq, int64_t n, int64_t col, bool colok,
                                            int64_t r, double2 v) {
     if (colok && r >= 0 && r < n) {
@@ -85,68 +100,95 @@ __device__ __forceinline__ void store_pair(double *Q, int64_t ldq, int64_t n, in
     }
 }
 
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 template <int B8, int D, int CW, int NCT>
 struct DmmaCfg {
     static constexpr int LAM = B8 + 1;
     static constexpr int BLOB = 128 * LAM + 64;            // doubles per group
     static constexpr int NWARP = D * CW;
     static constexpr int THREADS = 32 * NWARP;
-    // shared memory: 2 stages x D blobs, 2 parities x D x CW x NCT hand-off chunks
-    static constexpr size_t SMEM_BLOBS = size_t(2) * D * BLOB * sizeof(double);
+    static constexpr int T = CW * NCT;                     // 8-column tiles per work item
+    static constexpr int STAGES = (D * BLOB * 8 * 3 <= 150 * 1024) ? 3 : 2;
+    // shared memory: STAGES x D blobs, 2 parities x D x CW x NCT hand-off chunks, barriers
+    static constexpr size_t SMEM_BLOBS = size_t(STAGES) * D * BLOB * sizeof(double);
     static constexpr size_t SMEM_HAND = size_t(2) * D * CW * NCT * 64 * sizeof(double);
-    static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + 64;
+    static constexpr size_t SMEM_INTAKE = size_t(2) * CW * NCT * 64 * sizeof(double);   // warp-0 HBM intake
+    static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
 };
 
+// Cross-pass progress word of a tile group: ((p+1) << 32) | e means pass p
+// has finalised every chunk >= C0 + 2 - e (e = 0xFFFFFFFF: pass p complete).
+constexpr uint64_t kPassDone = 0xFFFFFFFFull;
+
+// Persistent kernel: work item k = (pass p = k / NX, tile group x = k % NX) over depth block
+// [p*D, p*D + D) and tiles [x*T, x*T + T); CTA c takes items c, c + gridDim.x, ... in order.
+// Item (x, p) consumes the rows item (x, p-1) emits, gated by prog[x] (acquire/release), so
+// consecutive passes of one tile group pipeline across CTAs.  Deadlock-free: every item
+// waits only on an item with a smaller index, and the grid never exceeds co-residency.
 template <int B8, int D, int CW, int NCT>
 __global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT>::THREADS, 1)
 apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, double *Q, int64_t ldq,
-                  int tiles_per_cta) {
+                  uint64_t *prog) {
     using Cfg = DmmaCfg<B8, D, CW, NCT>;
     constexpr int LAM = Cfg::LAM;
     constexpr int BLOB = Cfg::BLOB;
+    constexpr int S = Cfg::STAGES;
+    constexpr int T = Cfg::T;
     constexpr int64_t B = 8 * B8;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *sblob = reinterpret_cast<double *>(smem_raw);                          // [2][D][BLOB]
+    double *sblob = reinterpret_cast<double *>(smem_raw);                          // [S][D][BLOB]
     double2 *shand = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS);      // [2][D][CW][NCT][32]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);
+    double2 *sintake = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);  // [2][CW][NCT][32]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND + Cfg::SMEM_INTAKE);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int d = warp / CW, cw = warp % CW;
     const int64_t M = num_depths(n, B);
     const int64_t C0 = (n - 2) >> 3;                       // top chunk of every depth's first window
     const int64_t ntile = (nev + 7) >> 3;
-    const int64_t tile_begin = (int64_t)blockIdx.x * tiles_per_cta;
-    const int64_t tile_end = min(ntile, tile_begin + tiles_per_cta);
-
-    int64_t col[NCT];
-    bool colok[NCT], tileok[NCT];
-#pragma unroll
-    for (int t = 0; t < NCT; t++) {
-        const int64_t tile = tile_begin + cw * NCT + t;
-        tileok[t] = tile < tile_end;
-        col[t] = tile * 8 + (lane >> 2);
-        colok[t] = tileok[t] && col[t] < nev;
-    }
+    const int64_t NX = (ntile + T - 1) / T;
+    const int64_t NP = (M + D - 1) / D;
     const int rsub = 2 * (lane & 3);
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int i = 0; i < S; i++) mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    uint32_t phase_bits = 0;  // parity of the next completion, per stage (used by all threads)
+    uint32_t phase_bits = 0;  // parity of the next completion, per stage (all threads track it)
+    int64_t gstep = 0;        // global step counter (selects the ring stage)
 
-    for (int64_t m0 = 0; m0 < M; m0 += D) {
-        const int64_t G = groups_at_depth(n, B8, m0);      // groups of depth m0
-        const int64_t dmax = min((int64_t)D, M - m0) - 1;  // deepest existing depth in this pass
+    for (int64_t k = blockIdx.x; k < NX * NP; k += gridDim.x) {
+        const int64_t p = k / NX, x = k % NX;
+        const int64_t m0 = p * D;
+        const int64_t tile_end = min(ntile, (x + 1) * T);
+        int64_t col[NCT];
+        bool colok[NCT], tileok[NCT];
+#pragma unroll
+        for (int t = 0; t < NCT; t++) {
+            const int64_t tile = x * T + cw * NCT + t;
+            tileok[t] = tile < tile_end;
+            col[t] = tile * 8 + (lane >> 2);
+            colok[t] = tileok[t] && col[t] < nev;
+        }
+        const int64_t G = groups_at_depth(n, B8, m0);
+        const int64_t dmax = min((int64_t)D, M - m0) - 1;
         const int64_t nsteps = G + dmax;
+        const int64_t gbase = gstep;
 
-        // producer: prefetch the fragments of step `st` into stage st&1
-        auto issue = [&](int64_t st) {
-            uint64_t *bar = &bars[st & 1];
+        auto issue = [&](int64_t st) {  // fragments of item step st -> ring stage (gbase+st) % S
+            const int64_t gs = gbase + st;
+            uint64_t *bar = &bars[gs % S];
             uint32_t bytes = 0;
             for (int dd = 0; dd <= dmax; dd++) {
                 const int64_t g = G - 1 - st + dd;
@@ -157,32 +199,56 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
                 const int64_t g = G - 1 - st + dd;
                 if (g >= 0 && g < groups_at_depth(n, B8, m0 + dd)) {
                     const double *src = blobs + (group_base(n, B8, m0 + dd) + g) * BLOB;
-                    bulk_g2s(sblob + ((st & 1) * D + dd) * BLOB, src, BLOB * 8, bar);
+                    bulk_g2s(sblob + ((gs % S) * D + dd) * BLOB, src, BLOB * 8, bar);
                 }
             }
         };
-        if (threadIdx.x == 0) issue(0);
+        if (threadIdx.x == 0)
+            for (int st = 0; st < S - 1 && st < nsteps; st++) issue(st);
 
-        // initial windows: chunks [C0 + d*LAM, C0 + (d+1)*LAM) (only real rows are loaded)
+        // cross-pass dependency (warp 0 only): chunk c must be final from pass p-1
+        uint64_t seen = 0;
+        auto await_chunk = [&](int64_t c) {
+            if (p == 0 || c < 0) return;
+            const uint64_t need = (uint64_t(p) << 32) | uint64_t(C0 + 2 - c);
+            if (seen >= need) return;
+            if (lane == 0) {
+                uint64_t v = ld_acquire_u64(prog + x);
+                while (v < need) {
+                    __nanosleep(128);
+                    v = ld_acquire_u64(prog + x);
+                }
+                seen = v;
+            }
+            seen = __shfl_sync(0xffffffffu, seen, 0);
+        };
+
         double2 q[NCT][LAM];
+        if (d == 0) await_chunk(C0);
 #pragma unroll
         for (int t = 0; t < NCT; t++)
 #pragma unroll
             for (int i = 0; i < LAM; i++)
                 q[t][i] = load_pair(Q, ldq, n, col[t], colok[t], 8 * (C0 + d * LAM + i) + rsub);
 
-        double2 nxt[NCT];  // warp 0's prefetched next top chunk
-        for (int64_t st = 0; st < nsteps; st++) {
-            if (threadIdx.x == 0 && st + 1 < nsteps) issue(st + 1);
-            if (d == 0) {
+        // warp 0 streams its new top chunks HBM -> shared (cp.async, 2 slots, one step ahead):
+        // the chunk entering at the end of step st is C0 - st - 1, in slot st & 1
+        auto intake = [&](int64_t st) {
+            const int64_t c = C0 - st - 1;
+            await_chunk(c);
 #pragma unroll
-                for (int t = 0; t < NCT; t++)
-                    nxt[t] = load_pair(Q, ldq, n, col[t], colok[t], 8 * (C0 - st - 1) + rsub);
-            }
-            const int64_t md = m0 + d;
+            for (int t = 0; t < NCT; t++)
+                load_pair_async(&sintake[(((st & 1) * CW + cw) * NCT + t) * 32 + lane], Q, ldq, n, col[t], colok[t],
+                                8 * c + rsub);
+            cp_async_commit();
+        };
+        if (d == 0) intake(0);
+        for (int64_t st = 0; st < nsteps; st++) {
+            if (threadIdx.x == 0 && st + S - 1 < nsteps) issue(st + S - 1);
+            if (d == 0 && st + 1 < nsteps) intake(st + 1);
             const int64_t g = G - 1 - st + d;
-            const bool active = (d <= dmax) && g >= 0 && g < groups_at_depth(n, B8, md);
-            const uint32_t stage = st & 1;
+            const bool active = (d <= dmax) && g >= 0 && g < groups_at_depth(n, B8, m0 + d);
+            const uint32_t stage = uint32_t((gbase + st) % S);
             const uint32_t par = (phase_bits >> stage) & 1u;
             phase_bits ^= (1u << stage);
             if (active) {
@@ -190,28 +256,41 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
                 const double2 *dotB = reinterpret_cast<const double2 *>(sblob + (stage * D + d) * BLOB);
                 const double2 *updB = dotB + 32 * LAM;
                 const double2 tf = dotB[64 * LAM + lane];
-                double2 y0[NCT], y1[NCT];
+                // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1,
+                // chunk parity) so every warp keeps >= 4 DMMA chains in flight
+                constexpr int NACC = (NCT >= 2) ? 2 : 4;
+                double2 y[NCT][NACC];
 #pragma unroll
-                for (int t = 0; t < NCT; t++) { y0[t] = make_double2(0.0, 0.0); y1[t] = make_double2(0.0, 0.0); }
+                for (int t = 0; t < NCT; t++)
+#pragma unroll
+                    for (int a = 0; a < NACC; a++) y[t][a] = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int i = 0; i < LAM; i++) {
                     const double2 vb = dotB[i * 32 + lane];
 #pragma unroll
                     for (int t = 0; t < NCT; t++) {
                         if (!tileok[t]) continue;
-                        if (i & 1) { dmma(y1[t].x, y1[t].y, q[t][i].x, vb.x); dmma(y1[t].x, y1[t].y, q[t][i].y, vb.y); }
-                        else       { dmma(y0[t].x, y0[t].y, q[t][i].x, vb.x); dmma(y0[t].x, y0[t].y, q[t][i].y, vb.y); }
+                        double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
+                        double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
+                        dmma(ya.x, ya.y, q[t][i].x, vb.x);
+                        dmma(yb.x, yb.y, q[t][i].y, vb.y);
                     }
                 }
+                // W^T = Y^T (-T)
                 double2 w[NCT];
 #pragma unroll
                 for (int t = 0; t < NCT; t++) {
                     if (!tileok[t]) continue;
-                    const double ya = y0[t].x + y1[t].x, yb = y0[t].y + y1[t].y;
+                    double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
+                    if (NACC == 4) {
+                        ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
+                        yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
+                    }
                     w[t] = make_double2(0.0, 0.0);
                     dmma(w[t].x, w[t].y, ya, tf.x);
                     dmma(w[t].x, w[t].y, yb, tf.y);
                 }
+                // Q_W^T += W^T V_g^T
 #pragma unroll
                 for (int i = 0; i < LAM; i++) {
                     const double2 ub = updB[i * 32 + lane];
@@ -224,23 +303,33 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
                 }
             }
             if (st + 1 == nsteps) break;  // final windows are written back below
-            // emit the bottom chunk
             const int64_t cbot = C0 - st + d * LAM + LAM - 1;
             if (d == D - 1) {
 #pragma unroll
                 for (int t = 0; t < NCT; t++) store_pair(Q, ldq, n, col[t], colok[t], 8 * cbot + rsub, q[t][LAM - 1]);
+                if ((st & 3) == 3 && cbot <= C0 + 1 && cbot >= 0) {
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release_u64(prog + x, (uint64_t(p + 1) << 32) | uint64_t(C0 + 2 - cbot));
+                }
             } else {
 #pragma unroll
                 for (int t = 0; t < NCT; t++)
                     shand[((((st & 1) * D + d + 1) * CW + cw) * NCT + t) * 32 + lane] = q[t][LAM - 1];
             }
+            if (d == 0) {
+                if (st + 1 < nsteps) cp_async_wait<1>(); else cp_async_wait<0>();
+            }
             __syncthreads();
-            // shift the window down one chunk and take the new top chunk
 #pragma unroll
             for (int t = 0; t < NCT; t++) {
 #pragma unroll
                 for (int i = LAM - 1; i > 0; i--) q[t][i] = q[t][i - 1];
-                q[t][0] = (d == 0) ? nxt[t] : shand[((((st & 1) * D + d) * CW + cw) * NCT + t) * 32 + lane];
+                if (d == 0) {
+                    q[t][0] = sintake[(((st & 1) * CW + cw) * NCT + t) * 32 + lane];
+                } else {
+                    q[t][0] = shand[((((st & 1) * D + d) * CW + cw) * NCT + t) * 32 + lane];
+                }
             }
         }
         // write back the final windows (chunks [C0 - nsteps + 1 + d*LAM, ... + LAM))
@@ -249,7 +338,10 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
 #pragma unroll
             for (int i = 0; i < LAM; i++)
                 store_pair(Q, ldq, n, col[t], colok[t], 8 * (C0 - (nsteps - 1) + d * LAM + i) + rsub, q[t][i]);
-        __syncthreads();  // this pass's stores precede the next pass's loads
+        __threadfence();
+        __syncthreads();  // item complete: publish, and the smem ring/hand-off are free again
+        if (threadIdx.x == 0) st_release_u64(prog + x, (uint64_t(p + 1) << 32) | kPassDone);
+        gstep += nsteps;
     }
 }
 

@@ -77,7 +77,7 @@ def test_validation_order_before_device():
     assert _call(10, 4, 5, FAKE, FAKE, None, 10) == eb.ERR_NULL
     assert _call(11, 4, 5, FAKE, FAKE, FAKE, 11) == eb.ERR_ALIGN        # ldq odd
     assert _call(10, 4, 5, FAKE, FAKE, ctypes.c_void_p(0x10008), 10) == eb.ERR_ALIGN
-    assert _call(10, 8, 5, FAKE, FAKE, FAKE, 10, dict(kernel=2, depth_warps=3, col_warps=1, tiles_per_warp=1)) == eb.ERR_ARG
+    assert _call(10, 8, 5, FAKE, FAKE, FAKE, 10, dict(kernel=2, depth_warps=3, col_warps=1, tiles_per_warp=1, grid_ctas=0)) == eb.ERR_ARG
     assert _call(10, 6, 5, FAKE, FAKE, FAKE, 10, dict(kernel=2)) == eb.ERR_ARG   # DMMA needs nbw % 8 == 0
     assert _call(10, 8, 5, FAKE, FAKE, FAKE, 10, dict(kernel=7)) == eb.ERR_ARG
 

@@ -59,7 +59,7 @@ def test_reference_kernel_bitwise_real_C1(eb):
 
 
 # ------------------------------------------------------------------ DMMA kernel: tolerance
-SHAPES = [(1, 10, 2), (2, 4, 2), (4, 2, 2), (8, 1, 2), (4, 4, 1), (8, 2, 1), (2, 8, 1), (1, 16, 1)]
+SHAPES = [(1, 8, 2), (2, 4, 2), (2, 2, 4), (4, 2, 2), (4, 2, 4), (4, 1, 4), (8, 1, 2), (8, 1, 4), (4, 4, 1), (8, 2, 1)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -69,10 +69,12 @@ def test_dmma_all_shapes(eb, shape, nbw):
     n, nev = 301, 45                          # ragged: n odd, nev not a multiple of 8
     hv, tau, s, L, Q = synth_case(n, nbw, nev, nbw * 13 + D, ldq=302)
     want = oracle.apply(hv, tau, s, L, Q)
-    for tpc in sorted({1, CW * NCT, max(1, CW * NCT - 1)}):
+    # grid 1: one CTA runs every item in order; grid 2/3: passes of one tile group pipeline
+    # across CTAs through the progress words; 0: all co-resident CTAs
+    for grid in (0, 1, 2, 3):
         got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
-                                                         tiles_per_warp=NCT, tiles_per_cta=tpc))
-        assert _rel(got[:, :n], want[:, :n]) <= TOL, (shape, tpc)
+                                                         tiles_per_warp=NCT, grid_ctas=grid))
+        assert _rel(got[:, :n], want[:, :n]) <= TOL, (shape, grid)
         assert np.array_equal(got[:, n:], Q[:, n:])      # ldq padding untouched
 
 
@@ -125,7 +127,7 @@ def test_column_independence_bitwise(eb):
     for c0, c1 in [(0, 8), (3, 50), (77, 160), (159, 160)]:
         part = run_gpu(eb, n, nbw, hv, tau, Q[c0:c1].copy())
         assert np.array_equal(part, full[c0:c1]), (c0, c1)
-    alt = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=2, depth_warps=8, col_warps=1, tiles_per_warp=2))
+    alt = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=2, depth_warps=8, col_warps=1, tiles_per_warp=2, grid_ctas=5))
     assert np.array_equal(alt, full)
 
 

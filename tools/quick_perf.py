@@ -25,7 +25,7 @@ def bench(n, nbw, nev, opts, reps=3):
     return best, tprep, fl / best / 1e9
 
 cfgs = [(20000, 64, 20000), (20000, 64, 2000), (4096, 32, 4096)]
-shapes = [(1,10,2), (2,4,2), (4,2,2), (8,1,2), (4,4,1), (8,2,1), (2,8,1), (1,16,1)]
+shapes = [(1,8,2), (2,4,2), (2,2,4), (4,2,2), (4,2,4), (4,1,4), (8,1,2), (8,1,4), (4,4,1), (8,2,1)]
 for (n, nbw, nev) in cfgs:
     for sh in [None] + shapes:
         opts = None if sh is None else dict(kernel=2, depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2])
