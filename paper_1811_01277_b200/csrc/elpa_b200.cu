@@ -132,8 +132,8 @@ int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws,
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
 }
 
-// Co-resident grid of the persistent item kernel (every CTA must be resident at once:
-// items wait on items of lower index held by other CTAs).
+// Grid of the persistent item kernel: the co-resident maximum (more CTAs could not run
+// concurrently anyway; correctness does not depend on co-residency, see kernel_dmma.cuh).
 template <int B8, int D, int CW, int NCT>
 int64_t dmma_grid(const Plan &p) {
     auto kern = apply_dmma_kernel<B8, D, CW, NCT>;
@@ -154,9 +154,11 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     const int64_t grid = dmma_grid<B8, D, CW, NCT>(p);
     if (grid < 1) return ELPA_B200_ERR_CUDA;
     uint64_t *prog = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&prog), size_t(p.nx) * 8, s) != cudaSuccess) return ELPA_B200_ERR_CUDA;
+    // NX progress words + the work-item counter, zeroed per launch
+    const size_t pbytes = size_t(p.nx + 1) * 8;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return ELPA_B200_ERR_CUDA;
     int rc = ELPA_B200_OK;
-    if (cudaMemsetAsync(prog, 0, size_t(p.nx) * 8, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
         apply_dmma_kernel<B8, D, CW, NCT><<<unsigned(grid), DmmaCfg<B8, D, CW, NCT>::THREADS,
                                             DmmaCfg<B8, D, CW, NCT>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);

@@ -129,10 +129,11 @@ struct DmmaCfg {
 constexpr uint64_t kPassDone = 0xFFFFFFFFull;
 
 // Persistent kernel: work item k = (pass p = k / NX, tile group x = k % NX) over depth block
-// [p*D, p*D + D) and tiles [x*T, x*T + T); CTA c takes items c, c + gridDim.x, ... in order.
-// Item (x, p) consumes the rows item (x, p-1) emits, gated by prog[x] (acquire/release), so
-// consecutive passes of one tile group pipeline across CTAs.  Deadlock-free: every item
-// waits only on an item with a smaller index, and the grid never exceeds co-residency.
+// [p*D, p*D + D) and tiles [x*T, x*T + T).  CTAs dequeue items in increasing k from a global
+// counter (prog[NX]).  Item (x, p) consumes the rows item (x, p-1) emits, gated by prog[x]
+// (release/acquire), so consecutive passes of one tile group pipeline across CTAs.
+// Deadlock-free without any co-residency assumption: an item waits only on an item of
+// smaller index, which a running CTA dequeued earlier and finishes by induction.
 template <int B8, int D, int CW, int NCT>
 __global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT>::THREADS, 1)
 apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, double *Q, int64_t ldq,
@@ -167,8 +168,14 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
 
     uint32_t phase_bits = 0;  // parity of the next completion, per stage (all threads track it)
     int64_t gstep = 0;        // global step counter (selects the ring stage)
+    int64_t *s_item = reinterpret_cast<int64_t *>(bars + S);
 
-    for (int64_t k = blockIdx.x; k < NX * NP; k += gridDim.x) {
+    for (;;) {
+        if (threadIdx.x == 0)
+            *s_item = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(prog + NX), 1ull);
+        __syncthreads();
+        const int64_t k = *s_item;
+        if (k >= NX * NP) break;
         const int64_t p = k / NX, x = k % NX;
         const int64_t m0 = p * D;
         const int64_t tile_end = min(ntile, (x + 1) * T);
@@ -302,7 +309,10 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
                     }
                 }
             }
-            if (st + 1 == nsteps) break;  // final windows are written back below
+            if (st + 1 == nsteps) {       // final windows are written back below
+                if (d == 0) cp_async_wait<0>();   // drain the unused last intake before slot reuse
+                break;
+            }
             const int64_t cbot = C0 - st + d * LAM + LAM - 1;
             if (d == D - 1) {
 #pragma unroll

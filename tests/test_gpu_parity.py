@@ -174,3 +174,17 @@ def test_full_size_C3_sampled_columns(eb):
     Qs = np.concatenate([synthetic_q_np(n, c, c + 1, seed) for c in cols])
     want = oracle.apply(hv, tau, s, L, Qs)
     assert _rel(got, want) <= TOL
+
+
+@pytest.mark.parametrize("shape,grid", [((4, 2, 4), 7), ((4, 2, 4), 0), ((1, 8, 2), 5), ((8, 1, 2), 0),
+                                        ((2, 2, 4), 13), ((4, 1, 4), 3)])
+def test_multi_item_ctas_at_scale(eb, shape, grid):
+    """Many work items per CTA and passes of one tile group running concurrently on
+    different CTAs (progress words, slot reuse across items) — the regime of C2/C3."""
+    D, CW, NCT = shape
+    n, nbw, nev = 2000, 32, 520
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 31 + D * CW)
+    want = oracle.apply(hv, tau, s, L, Q)
+    got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
+                                                     tiles_per_warp=NCT, grid_ctas=grid))
+    assert _rel(got, want) <= TOL
