@@ -154,8 +154,8 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     const int64_t grid = dmma_grid<B8, D, CW, NCT>(p);
     if (grid < 1) return ELPA_B200_ERR_CUDA;
     uint64_t *prog = nullptr;
-    // NX progress words + the work-item counter, zeroed per launch
-    const size_t pbytes = size_t(p.nx + 1) * 8;
+    // one progress word per work item + the work-item counter, zeroed per launch
+    const size_t pbytes = size_t(p.items + 1) * 8;
     if (cudaMallocAsync(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return ELPA_B200_ERR_CUDA;
     int rc = ELPA_B200_OK;
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;

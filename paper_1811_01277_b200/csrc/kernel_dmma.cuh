@@ -124,14 +124,15 @@ struct DmmaCfg {
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
 };
 
-// Cross-pass progress word of a tile group: ((p+1) << 32) | e means pass p
-// has finalised every chunk >= C0 + 2 - e (e = 0xFFFFFFFF: pass p complete).
-constexpr uint64_t kPassDone = 0xFFFFFFFFull;
+// Progress word of work item (x, p): e means pass p of tile group x has
+// finalised every chunk >= C0 + 2 - e (kPassDone: the item is complete).  One word per item:
+// a word shared by the passes of a tile group would be overwritten by the consumer itself.
+constexpr uint64_t kPassDone = ~0ull;
 
 // Persistent kernel: work item k = (pass p = k / NX, tile group x = k % NX) over depth block
 // [p*D, p*D + D) and tiles [x*T, x*T + T).  CTAs dequeue items in increasing k from a global
-// counter (prog[NX]).  Item (x, p) consumes the rows item (x, p-1) emits, gated by prog[x]
-// (release/acquire), so consecutive passes of one tile group pipeline across CTAs.
+// counter (prog[NX*NP]).  Item (x, p) consumes the rows item (x, p-1) emits, gated by
+// prog[k - NX] (release/acquire), so consecutive passes of one tile group pipeline across CTAs.
 // Deadlock-free without any co-residency assumption: an item waits only on an item of
 // smaller index, which a running CTA dequeued earlier and finishes by induction.
 template <int B8, int D, int CW, int NCT>
@@ -172,7 +173,7 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
 
     for (;;) {
         if (threadIdx.x == 0)
-            *s_item = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(prog + NX), 1ull);
+            *s_item = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(prog + NX * NP), 1ull);
         __syncthreads();
         const int64_t k = *s_item;
         if (k >= NX * NP) break;
@@ -217,13 +218,13 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
         uint64_t seen = 0;
         auto await_chunk = [&](int64_t c) {
             if (p == 0 || c < 0) return;
-            const uint64_t need = (uint64_t(p) << 32) | uint64_t(C0 + 2 - c);
+            const uint64_t need = uint64_t(C0 + 2 - c);
             if (seen >= need) return;
             if (lane == 0) {
-                uint64_t v = ld_acquire_u64(prog + x);
+                uint64_t v = ld_acquire_u64(prog + (k - NX));
                 while (v < need) {
                     __nanosleep(128);
-                    v = ld_acquire_u64(prog + x);
+                    v = ld_acquire_u64(prog + (k - NX));
                 }
                 seen = v;
             }
@@ -320,7 +321,7 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
                 if ((st & 3) == 3 && cbot <= C0 + 1 && cbot >= 0) {
                     __threadfence();
                     __syncwarp();
-                    if (lane == 0) st_release_u64(prog + x, (uint64_t(p + 1) << 32) | uint64_t(C0 + 2 - cbot));
+                    if (lane == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
                 }
             } else {
 #pragma unroll
@@ -350,7 +351,7 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
                 store_pair(Q, ldq, n, col[t], colok[t], 8 * (C0 - (nsteps - 1) + d * LAM + i) + rsub, q[t][i]);
         __threadfence();
         __syncthreads();  // item complete: publish, and the smem ring/hand-off are free again
-        if (threadIdx.x == 0) st_release_u64(prog + x, (uint64_t(p + 1) << 32) | kPassDone);
+        if (threadIdx.x == 0) st_release_u64(prog + k, kPassDone);
         gstep += nsteps;
     }
 }
