@@ -60,17 +60,14 @@ size_t dmma_smem(int b8, int D, int CW, int NCT) {
     return size_t(stages) * D * blob * 8 + size_t(2) * D * CW * NCT * 64 * 8 + size_t(2) * CW * NCT * 64 * 8 + 64;
 }
 
-// Automatic choice: D = 4 pipelined depths per work item (HBM traffic for Q
-// is 1/D of a depth-at-a-time sweep), 8 tiles (64 columns) per item so each prepared
-// fragment block in shared memory serves 8 tiles, 2 warps per SMSP; work items
-// (tile group, depth pass) are spread over all SMs, so balance no longer depends on
-// nev / (8 * #SMs).  Narrow problems use 4-tile items to keep >= ~8 items per SM.
+// Automatic choice (measured sweep in profiles/shape_sweep_r01.jsonl):
+// D = 2 pipelined depths per work item, 2 column warps x 4 tiles (64 columns per item),
+// 128 threads and ~83 KB shared memory per CTA so two CTAs share an SM and overlap each
+// other's per-step barriers.  Work items (tile group, depth pass) are spread dynamically
+// over all SMs, so balance no longer depends on nev / (8 * #SMs).
 void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT) {
-    const int sms = sm_count();
-    const int64_t np4 = (M + 3) / 4;
-    if (((ntile + 7) / 8) * np4 >= 8 * sms) { D = 4; CW = 2; NCT = 4; }
-    else { D = 4; CW = 1; NCT = 4; }
-    (void)b8;
+    (void)ntile; (void)M; (void)b8;
+    D = 2; CW = 2; NCT = 4;
 }
 
 int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
