@@ -81,6 +81,7 @@ typedef struct {
     int col_warps;       /* CW: warps splitting a work item's column stripe, 0 = auto */
     int tiles_per_warp;  /* NCT: 8-column tiles per warp (1,2,4); an item has CW*NCT tiles */
     int grid_ctas;       /* persistent CTAs to launch, 0 = all co-resident (148 x occupancy) */
+    int groups_per_step; /* K: reflector groups (of 8) per CTA barrier (1,2,4), 0 = auto */
 } elpa_b200_opts;
 
 /* R(n, nbw): number of reflectors the band->tridiagonal chase produces.
@@ -127,7 +128,7 @@ int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev,
                              const elpa_b200_opts *opts);
 
 /* Describe the launch the library would make for (n, nbw, nev, opts): writes
- * "kernel=... D=.. CW=.. NCT=.. items=.. grid_req=.. block=.. smem=.. ws=.." into buf.
+ * "kernel=... D=.. CW=.. NCT=.. K=.. items=.. grid_req=.. block=.. smem=.. ws=.." into buf.
  * Returns the number of kernel launches one elpa_trans_ev_tridi_to_band call makes, or a
  * negative code. */
 int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *opts,

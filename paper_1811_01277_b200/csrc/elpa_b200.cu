@@ -20,7 +20,7 @@ constexpr int kMaxSms = 148;
 
 struct Plan {
     int kernel = ELPA_B200_KERNEL_REFERENCE;
-    int b8 = 0, D = 1, CW = 1, NCT = 1;
+    int b8 = 0, D = 1, CW = 1, NCT = 1, K = 1;
     int grid_req = 0;          // requested grid (0 = co-resident maximum)
     int64_t items = 0;         // (tile group, depth pass) work items
     int64_t nx = 0;            // tile groups
@@ -43,21 +43,24 @@ bool b8_supported(int64_t nbw) {
 }
 
 // (D, CW, NCT) menu of compiled DMMA configurations
-struct Shape { int D, CW, NCT; };
-#define ELPA_SHAPES(X) X(1, 8, 2) X(2, 4, 2) X(2, 2, 4) X(4, 2, 2) X(4, 2, 4) X(4, 1, 4) X(8, 1, 2) X(8, 1, 4) X(4, 4, 1) X(8, 2, 1)
-#define ELPA_SHAPE_ENTRY(D_, CW_, NCT_) {D_, CW_, NCT_},
+// (D depth warps, CW column warps, NCT tiles per warp, K groups per step)
+struct Shape { int D, CW, NCT, K; };
+#define ELPA_SHAPES(X) X(1, 2, 4, 1) X(1, 2, 4, 2) X(2, 2, 4, 1) X(2, 2, 4, 2) X(2, 2, 4, 4) X(4, 2, 4, 1) \
+    X(4, 2, 4, 2) X(4, 1, 4, 2) X(8, 1, 4, 1) X(2, 4, 2, 1) X(2, 4, 2, 2) X(2, 2, 3, 1) X(2, 2, 3, 2)
+#define ELPA_SHAPE_ENTRY(D_, CW_, NCT_, K_) {D_, CW_, NCT_, K_},
 constexpr Shape kShapes[] = {ELPA_SHAPES(ELPA_SHAPE_ENTRY)};
 
-bool shape_compiled(int D, int CW, int NCT) {
+bool shape_compiled(int D, int CW, int NCT, int K) {
     for (const Shape &s : kShapes)
-        if (s.D == D && s.CW == CW && s.NCT == NCT) return true;
+        if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
     return false;
 }
 
-size_t dmma_smem(int b8, int D, int CW, int NCT) {
+size_t dmma_smem(int b8, int D, int CW, int NCT, int K) {
     const size_t blob = size_t(128) * (b8 + 1) + 64;
-    const int stages = (D * blob * 8 * 3 <= 150 * 1024) ? 3 : 2;
-    return size_t(stages) * D * blob * 8 + size_t(2) * D * CW * NCT * 64 * 8 + size_t(2) * CW * NCT * 64 * 8 + 64;
+    const int stages = (K * D * blob * 8 * 3 <= 100 * 1024) ? 3 : 2;
+    return size_t(stages) * K * D * blob * 8 + size_t(2) * D * K * CW * NCT * 64 * 8 +
+           size_t(2) * K * CW * NCT * 64 * 8 + 64;
 }
 
 // Automatic choice (measured sweep in profiles/shape_sweep_r01.jsonl):
@@ -65,9 +68,9 @@ size_t dmma_smem(int b8, int D, int CW, int NCT) {
 // 128 threads and ~83 KB shared memory per CTA so two CTAs share an SM and overlap each
 // other's per-step barriers.  Work items (tile group, depth pass) are spread dynamically
 // over all SMs, so balance no longer depends on nev / (8 * #SMs).
-void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT) {
+void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int &K) {
     (void)ntile; (void)M; (void)b8;
-    D = 2; CW = 2; NCT = 4;
+    D = 2; CW = 2; NCT = 4; K = 1;
 }
 
 int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
@@ -87,16 +90,22 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     const int64_t ntile = (nev + 7) / 8;
     const int64_t M = num_depths(n, nbw);
     int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NCT = o ? o->tiles_per_warp : 0;
-    if (D == 0 && CW == 0 && NCT == 0) auto_shape(ntile, M, p.b8, D, CW, NCT);
-    if (!shape_compiled(D, CW, NCT)) return ELPA_B200_ERR_ARG;
-    p.D = D; p.CW = CW; p.NCT = NCT;
+    int K = o ? o->groups_per_step : 0;
+    if (D == 0 && CW == 0 && NCT == 0) {
+        int Ka = 0;
+        auto_shape(ntile, M, p.b8, D, CW, NCT, Ka);
+        if (K == 0) K = Ka;
+    }
+    if (K == 0) K = 1;
+    if (!shape_compiled(D, CW, NCT, K)) return ELPA_B200_ERR_ARG;
+    p.D = D; p.CW = CW; p.NCT = NCT; p.K = K;
     p.grid_req = o ? o->grid_ctas : 0;
     if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
     p.nx = (ntile + CW * NCT - 1) / (CW * NCT);
     p.items = p.nx * ((M + D - 1) / D);
     p.grid = p.items;          // capped by co-residency at launch
     p.threads = 32 * D * CW;
-    p.smem = dmma_smem(p.b8, D, CW, NCT);
+    p.smem = dmma_smem(p.b8, D, CW, NCT, K);
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1) * 8 : 0;
     return ELPA_B200_OK;
 }
@@ -131,13 +140,13 @@ int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws,
 
 // Grid of the persistent item kernel: the co-resident maximum (more CTAs could not run
 // concurrently anyway; correctness does not depend on co-residency, see kernel_dmma.cuh).
-template <int B8, int D, int CW, int NCT>
+template <int B8, int D, int CW, int NCT, int K>
 int64_t dmma_grid(const Plan &p) {
-    auto kern = apply_dmma_kernel<B8, D, CW, NCT>;
-    const size_t smem = DmmaCfg<B8, D, CW, NCT>::SMEM;
+    auto kern = apply_dmma_kernel<B8, D, CW, NCT, K>;
+    const size_t smem = DmmaCfg<B8, D, CW, NCT, K>::SMEM;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<B8, D, CW, NCT>::THREADS, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<B8, D, CW, NCT, K>::THREADS, smem) !=
             cudaSuccess || per_sm < 1)
         return -1;
     int64_t g = int64_t(per_sm) * sm_count();
@@ -145,10 +154,10 @@ int64_t dmma_grid(const Plan &p) {
     return g < p.items ? g : p.items;
 }
 
-template <int B8, int D, int CW, int NCT>
+template <int B8, int D, int CW, int NCT, int K>
 int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
                       cudaStream_t s) {
-    const int64_t grid = dmma_grid<B8, D, CW, NCT>(p);
+    const int64_t grid = dmma_grid<B8, D, CW, NCT, K>(p);
     if (grid < 1) return ELPA_B200_ERR_CUDA;
     uint64_t *prog = nullptr;
     // one progress word per work item + the work-item counter, zeroed per launch
@@ -157,8 +166,8 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     int rc = ELPA_B200_OK;
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
-        apply_dmma_kernel<B8, D, CW, NCT><<<unsigned(grid), DmmaCfg<B8, D, CW, NCT>::THREADS,
-                                            DmmaCfg<B8, D, CW, NCT>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
+        apply_dmma_kernel<B8, D, CW, NCT, K><<<unsigned(grid), DmmaCfg<B8, D, CW, NCT, K>::THREADS,
+                                               DmmaCfg<B8, D, CW, NCT, K>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     }
     if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
@@ -168,8 +177,9 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
 template <int B8>
 int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
                    cudaStream_t s) {
-#define ELPA_SHAPE(D_, CW_, NCT_) \
-    if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_) return launch_dmma_shape<B8, D_, CW_, NCT_>(p, n, nev, ws, Q, ldq, s);
+#define ELPA_SHAPE(D_, CW_, NCT_, K_)                          \
+    if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
+        return launch_dmma_shape<B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
     ELPA_SHAPES(ELPA_SHAPE)
 #undef ELPA_SHAPE
     return ELPA_B200_ERR_ARG;
@@ -238,8 +248,8 @@ int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts
     int rc = make_plan(n, nbw, nev, opts, p);
     if (rc != ELPA_B200_OK) return rc;
     if (buf && buflen)
-        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NCT=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
-                 p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : "reference", p.b8, p.D, p.CW, p.NCT, (long long)p.items,
+        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NCT=%d K=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
+                 p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : "reference", p.b8, p.D, p.CW, p.NCT, p.K, (long long)p.items,
                  p.grid_req, p.threads, p.smem, (long long)p.ws_bytes);
     if (hh_total(n, nbw) == 0 || nev == 0) return 0;
     return p.kernel == ELPA_B200_KERNEL_DMMA ? 2 : 1;

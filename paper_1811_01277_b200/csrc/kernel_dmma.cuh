@@ -68,35 +68,24 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Q chunk I/O: lane owns rows r, r+1 (r = 8*chunk + 2*(lane%4)) of column `col`.
-__device__ __forceinline__ double2 load_pair(const double *Q, int64_t ldq, int64_t n, int64_t col,
-                                             bool colok, int64_t r) {
+// Q chunk I/O: lane owns rows r, r+1 (r = 8*chunk + 2*(lane%4)) of the column starting at
+// `colp`; rows outside [0, n) and masked-off columns read as zero and are never written.
+__device__ __forceinline__ double2 load_pair(const double *colp, bool ok, int n, int r) {
     double2 v = make_double2(0.0, 0.0);
-    if (colok && r >= 0 && r < n) {
-        const double *p = Q + col * ldq + r;
-        if (r + 1 < n) {
-            v = *reinterpret_cast<const double2 *>(p);
-        } else {
-            v.x = p[0];
-        }
+    if (ok && r >= 0 && r < n) {
+        if (r + 1 < n) v = *reinterpret_cast<const double2 *>(colp + r);
+        else v.x = colp[r];
     }
     return v;
 }
-__device__ __forceinline__ void load_pair_async(double2 *dst, const double *Q, int64_t ldq, int64_t n, int64_t col,
-                                                bool colok, int64_t r) {
-    const bool ok = colok && r >= 0 && r < n;
-    const double *src = ok ? Q + col * ldq + r : Q;
-    cp_async16_zfill(dst, src, ok ? (r + 1 < n ? 16u : 8u) : 0u);
+__device__ __forceinline__ void load_pair_async(double2 *dst, const double *colp, bool ok, int n, int r) {
+    const bool in = ok && r >= 0 && r < n;
+    cp_async16_zfill(dst, in ? colp + r : colp, in ? (r + 1 < n ? 16u : 8u) : 0u);
 }
-__device__ __forceinline__ void store_pair(double *Q, int64_t ldq, int64_t n, int64_t col, bool colok,
-                                           int64_t r, double2 v) {
-    if (colok && r >= 0 && r < n) {
-        double *p = Q + col * ldq + r;
-        if (r + 1 < n) {
-            *reinterpret_cast<double2 *>(p) = v;
-        } else {
-            p[0] = v.x;
-        }
+__device__ __forceinline__ void store_pair(double *colp, bool ok, int n, int r, double2 v) {
+    if (ok && r >= 0 && r < n) {
+        if (r + 1 < n) *reinterpret_cast<double2 *>(colp + r) = v;
+        else colp[r] = v.x;
     }
 }
 
@@ -109,18 +98,19 @@ __device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
     asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <int B8, int D, int CW, int NCT>
+template <int B8, int D, int CW, int NCT, int K>
 struct DmmaCfg {
     static constexpr int LAM = B8 + 1;
     static constexpr int BLOB = 128 * LAM + 64;            // doubles per group
     static constexpr int NWARP = D * CW;
     static constexpr int THREADS = 32 * NWARP;
     static constexpr int T = CW * NCT;                     // 8-column tiles per work item
-    static constexpr int STAGES = (D * BLOB * 8 * 3 <= 150 * 1024) ? 3 : 2;
-    // shared memory: STAGES x D blobs, 2 parities x D x CW x NCT hand-off chunks, barriers
-    static constexpr size_t SMEM_BLOBS = size_t(STAGES) * D * BLOB * sizeof(double);
-    static constexpr size_t SMEM_HAND = size_t(2) * D * CW * NCT * 64 * sizeof(double);
-    static constexpr size_t SMEM_INTAKE = size_t(2) * CW * NCT * 64 * sizeof(double);   // warp-0 HBM intake
+    static constexpr int STAGES = (K * D * BLOB * 8 * 3 <= 100 * 1024) ? 3 : 2;
+    // shared memory: STAGES x K x D fragment blobs, hand-off chunks [2][D][K][CW][NCT][32],
+    // warp-0 intake chunks [2][K][CW][NCT][32], barriers + the dequeued item index
+    static constexpr size_t SMEM_BLOBS = size_t(STAGES) * K * D * BLOB * sizeof(double);
+    static constexpr size_t SMEM_HAND = size_t(2) * D * K * CW * NCT * 64 * sizeof(double);
+    static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
 };
 
@@ -135,31 +125,47 @@ constexpr uint64_t kPassDone = ~0ull;
 // prog[k - NX] (release/acquire), so consecutive passes of one tile group pipeline across CTAs.
 // Deadlock-free without any co-residency assumption: an item waits only on an item of
 // smaller index, which a running CTA dequeued earlier and finishes by induction.
-template <int B8, int D, int CW, int NCT>
-__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT>::THREADS, 1)
-apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, double *Q, int64_t ldq,
+//
+// Inside an item, group-time tau = 0, 1, ...: depth warp d applies group
+// g = G - 1 - tau + d*(K+1) of depth m0 + d; its window's top chunk is C0 - tau + d*(LAM + K).
+// Depth m0+d+1 trails depth m0+d by K+1 groups, so the chunk warp d takes in after tau was
+// emitted by warp d-1 after tau - K, i.e. in the previous step: the K chunks between two
+// windows are in transit in shared memory.  One step = K group-times = one CTA barrier.
+template <int B8, int D, int CW, int NCT, int K>
+__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT, K>::THREADS, 1)
+apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, double *Q, int64_t ldq,
                   uint64_t *prog) {
-    using Cfg = DmmaCfg<B8, D, CW, NCT>;
+    using Cfg = DmmaCfg<B8, D, CW, NCT, K>;
     constexpr int LAM = Cfg::LAM;
     constexpr int BLOB = Cfg::BLOB;
     constexpr int S = Cfg::STAGES;
     constexpr int T = Cfg::T;
-    constexpr int64_t B = 8 * B8;
+    constexpr int B = 8 * B8;
+    constexpr int LAG = K + 1;                             // groups depth m+1 trails depth m
+    constexpr int SPAN = LAM + K;                          // chunk distance between stacked windows
+    constexpr int PUB = (K >= 4) ? 4 : 16 / K;             // publish progress every PUB steps
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *sblob = reinterpret_cast<double *>(smem_raw);                          // [S][D][BLOB]
-    double2 *shand = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS);      // [2][D][CW][NCT][32]
-    double2 *sintake = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);  // [2][CW][NCT][32]
+    double *sblob = reinterpret_cast<double *>(smem_raw);                                        // [S][K][D][BLOB]
+    double2 *shand = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS);                    // [2][D][K][CW][NCT][32]
+    double2 *sintake = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);  // [2][K][CW][NCT][32]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND + Cfg::SMEM_INTAKE);
+    int *s_item = reinterpret_cast<int *>(bars + S);
 
+    const int n = int(n64), nev = int(nev64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int d = warp / CW, cw = warp % CW;
-    const int64_t M = num_depths(n, B);
-    const int64_t C0 = (n - 2) >> 3;                       // top chunk of every depth's first window
-    const int64_t ntile = (nev + 7) >> 3;
-    const int64_t NX = (ntile + T - 1) / T;
-    const int64_t NP = (M + D - 1) / D;
+    const int M = int(num_depths(n64, B));
+    const int C0 = (n - 2) >> 3;                           // top chunk of every depth's first window
+    const int ntile = (nev + 7) >> 3;
+    const int NX = (ntile + T - 1) / T;
+    const int NP = (M + D - 1) / D;
     const int rsub = 2 * (lane & 3);
+    // hand-off / intake slot of (parity, j, t) for this lane
+    auto hslot = [&](int par, int dd, int j, int t) {
+        return ((((par * D + dd) * K + j) * CW + cw) * NCT + t) * 32 + lane;
+    };
+    auto islot = [&](int par, int j, int t) { return (((par * K + j) * CW + cw) * NCT + t) * 32 + lane; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; i++) mbar_init(&bars[i], 1);
@@ -168,57 +174,60 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
     __syncthreads();
 
     uint32_t phase_bits = 0;  // parity of the next completion, per stage (all threads track it)
-    int64_t gstep = 0;        // global step counter (selects the ring stage)
-    int64_t *s_item = reinterpret_cast<int64_t *>(bars + S);
+    int stage0 = 0;           // ring stage of the item's step 0
 
     for (;;) {
         if (threadIdx.x == 0)
-            *s_item = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(prog + NX * NP), 1ull);
+            *s_item = int(atomicAdd(reinterpret_cast<unsigned long long *>(prog + int64_t(NX) * NP), 1ull));
         __syncthreads();
-        const int64_t k = *s_item;
+        const int k = *s_item;
         if (k >= NX * NP) break;
-        const int64_t p = k / NX, x = k % NX;
-        const int64_t m0 = p * D;
-        const int64_t tile_end = min(ntile, (x + 1) * T);
-        int64_t col[NCT];
-        bool colok[NCT], tileok[NCT];
+        const int p = k / NX, x = k % NX;
+        const int m0 = p * D;
+        const int tile_end = min(ntile, (x + 1) * T);
+        double *qcol[NCT];
+        uint32_t okmask = 0, tilemask = 0;
 #pragma unroll
         for (int t = 0; t < NCT; t++) {
-            const int64_t tile = x * T + cw * NCT + t;
-            tileok[t] = tile < tile_end;
-            col[t] = tile * 8 + (lane >> 2);
-            colok[t] = tileok[t] && col[t] < nev;
+            const int tile = x * T + cw * NCT + t;
+            const int c = tile * 8 + (lane >> 2);
+            if (tile < tile_end) tilemask |= 1u << t;
+            if (tile < tile_end && c < nev) okmask |= 1u << t;
+            qcol[t] = Q + int64_t(min(c, nev - 1)) * ldq;
         }
-        const int64_t G = groups_at_depth(n, B8, m0);
-        const int64_t dmax = min((int64_t)D, M - m0) - 1;
-        const int64_t nsteps = G + dmax;
-        const int64_t gbase = gstep;
+        const int G = int(groups_at_depth(n64, B8, m0));
+        const int dmax = min(D, M - m0) - 1;
+        const int NT = G + dmax * LAG;                     // group-times of this item
+        const int nsteps = (NT + K - 1) / K;
 
-        auto issue = [&](int64_t st) {  // fragments of item step st -> ring stage (gbase+st) % S
-            const int64_t gs = gbase + st;
-            uint64_t *bar = &bars[gs % S];
+        auto group_valid = [&](int tau, int dd) {
+            const int g = G - 1 - tau + dd * LAG;
+            return dd <= dmax && tau < NT && g >= 0 && g < G - dd * B8;
+        };
+        auto issue = [&](int st) {  // fragments of step st -> ring stage (stage0 + st) % S
+            const int stg = (stage0 + st) % S;
+            uint64_t *bar = &bars[stg];
             uint32_t bytes = 0;
-            for (int dd = 0; dd <= dmax; dd++) {
-                const int64_t g = G - 1 - st + dd;
-                if (g >= 0 && g < groups_at_depth(n, B8, m0 + dd)) bytes += BLOB * 8;
-            }
+            for (int j = 0; j < K; j++)
+                for (int dd = 0; dd <= dmax; dd++)
+                    if (group_valid(st * K + j, dd)) bytes += BLOB * 8;
             mbar_arrive_expect_tx(bar, bytes);
-            for (int dd = 0; dd <= dmax; dd++) {
-                const int64_t g = G - 1 - st + dd;
-                if (g >= 0 && g < groups_at_depth(n, B8, m0 + dd)) {
-                    const double *src = blobs + (group_base(n, B8, m0 + dd) + g) * BLOB;
-                    bulk_g2s(sblob + ((gs % S) * D + dd) * BLOB, src, BLOB * 8, bar);
-                }
-            }
+            for (int j = 0; j < K; j++)
+                for (int dd = 0; dd <= dmax; dd++)
+                    if (group_valid(st * K + j, dd)) {
+                        const int g = G - 1 - (st * K + j) + dd * LAG;
+                        const double *src = blobs + (group_base(n64, B8, m0 + dd) + g) * BLOB;
+                        bulk_g2s(sblob + ((stg * K + j) * D + dd) * BLOB, src, BLOB * 8, bar);
+                    }
         };
         if (threadIdx.x == 0)
             for (int st = 0; st < S - 1 && st < nsteps; st++) issue(st);
 
         // cross-pass dependency (warp 0 only): chunk c must be final from pass p-1
-        uint64_t seen = 0;
-        auto await_chunk = [&](int64_t c) {
+        uint32_t seen = 0;
+        auto await_chunk = [&](int c) {
             if (p == 0 || c < 0) return;
-            const uint64_t need = uint64_t(C0 + 2 - c);
+            const uint32_t need = uint32_t(C0 + 2 - c);
             if (seen >= need) return;
             if (lane == 0) {
                 uint64_t v = ld_acquire_u64(prog + (k - NX));
@@ -226,9 +235,22 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
                     __nanosleep(128);
                     v = ld_acquire_u64(prog + (k - NX));
                 }
-                seen = v;
+                seen = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(v);
             }
             seen = __shfl_sync(0xffffffffu, seen, 0);
+        };
+        // warp 0 streams its new top chunks HBM -> shared (cp.async, one step ahead): the chunk
+        // entering after group-time tau = st*K + j is C0 - tau - 1, in slot [st & 1][j]
+        auto intake = [&](int st) {
+#pragma unroll
+            for (int j = 0; j < K; j++) {
+                const int c = C0 - (st * K + j) - 1;
+                await_chunk(c);
+#pragma unroll
+                for (int t = 0; t < NCT; t++)
+                    load_pair_async(&sintake[islot(st & 1, j, t)], qcol[t], (okmask >> t) & 1, n, 8 * c + rsub);
+            }
+            cp_async_commit();
         };
 
         double2 q[NCT][LAM];
@@ -237,122 +259,134 @@ apply_dmma_kernel(int64_t n, int64_t nev, const double *__restrict__ blobs, doub
         for (int t = 0; t < NCT; t++)
 #pragma unroll
             for (int i = 0; i < LAM; i++)
-                q[t][i] = load_pair(Q, ldq, n, col[t], colok[t], 8 * (C0 + d * LAM + i) + rsub);
-
-        // warp 0 streams its new top chunks HBM -> shared (cp.async, 2 slots, one step ahead):
-        // the chunk entering at the end of step st is C0 - st - 1, in slot st & 1
-        auto intake = [&](int64_t st) {
-            const int64_t c = C0 - st - 1;
-            await_chunk(c);
-#pragma unroll
-            for (int t = 0; t < NCT; t++)
-                load_pair_async(&sintake[(((st & 1) * CW + cw) * NCT + t) * 32 + lane], Q, ldq, n, col[t], colok[t],
-                                8 * c + rsub);
-            cp_async_commit();
-        };
+                q[t][i] = load_pair(qcol[t], (okmask >> t) & 1, n, 8 * (C0 + d * SPAN + i) + rsub);
         if (d == 0) intake(0);
-        for (int64_t st = 0; st < nsteps; st++) {
+
+        bool done = false;
+        for (int st = 0; !done; st++) {
             if (threadIdx.x == 0 && st + S - 1 < nsteps) issue(st + S - 1);
             if (d == 0 && st + 1 < nsteps) intake(st + 1);
-            const int64_t g = G - 1 - st + d;
-            const bool active = (d <= dmax) && g >= 0 && g < groups_at_depth(n, B8, m0 + d);
-            const uint32_t stage = uint32_t((gbase + st) % S);
+            const uint32_t stage = uint32_t((stage0 + st) % S);
             const uint32_t par = (phase_bits >> stage) & 1u;
             phase_bits ^= (1u << stage);
-            if (active) {
-                mbar_wait(&bars[stage], par);
-                const double2 *dotB = reinterpret_cast<const double2 *>(sblob + (stage * D + d) * BLOB);
-                const double2 *updB = dotB + 32 * LAM;
-                const double2 tf = dotB[64 * LAM + lane];
-                // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1,
-                // chunk parity) so every warp keeps >= 4 DMMA chains in flight
-                constexpr int NACC = (NCT >= 2) ? 2 : 4;
-                double2 y[NCT][NACC];
+            bool waited = false;
+#pragma unroll 1
+            for (int j = 0; j < K; j++) {
+                const int tau = st * K + j;
+                if (group_valid(tau, d)) {
+                    if (!waited) { mbar_wait(&bars[stage], par); waited = true; }
+                    const double2 *dotB = reinterpret_cast<const double2 *>(sblob + ((stage * K + j) * D + d) * BLOB);
+                    const double2 *updB = dotB + 32 * LAM;
+                    const double2 tf = dotB[64 * LAM + lane];
+                    // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1,
+                    // chunk parity) so every warp keeps >= 4 DMMA chains in flight
+                    constexpr int NACC = (NCT >= 2) ? 2 : 4;
+                    double2 y[NCT][NACC];
 #pragma unroll
-                for (int t = 0; t < NCT; t++)
+                    for (int t = 0; t < NCT; t++)
 #pragma unroll
-                    for (int a = 0; a < NACC; a++) y[t][a] = make_double2(0.0, 0.0);
+                        for (int a = 0; a < NACC; a++) y[t][a] = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int i = 0; i < LAM; i++) {
-                    const double2 vb = dotB[i * 32 + lane];
+                    for (int i = 0; i < LAM; i++) {
+                        const double2 vb = dotB[i * 32 + lane];
+#pragma unroll
+                        for (int t = 0; t < NCT; t++) {
+                            if (!((tilemask >> t) & 1)) continue;
+                            double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
+                            double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
+                            dmma(ya.x, ya.y, q[t][i].x, vb.x);
+                            dmma(yb.x, yb.y, q[t][i].y, vb.y);
+                        }
+                    }
+                    // W^T = Y^T (-T)
+                    double2 w[NCT];
 #pragma unroll
                     for (int t = 0; t < NCT; t++) {
-                        if (!tileok[t]) continue;
-                        double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
-                        double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
-                        dmma(ya.x, ya.y, q[t][i].x, vb.x);
-                        dmma(yb.x, yb.y, q[t][i].y, vb.y);
+                        if (!((tilemask >> t) & 1)) continue;
+                        double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
+                        if (NACC == 4) {
+                            ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
+                            yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
+                        }
+                        w[t] = make_double2(0.0, 0.0);
+                        dmma(w[t].x, w[t].y, ya, tf.x);
+                        dmma(w[t].x, w[t].y, yb, tf.y);
+                    }
+                    // Q_W^T += W^T V_g^T
+#pragma unroll
+                    for (int i = 0; i < LAM; i++) {
+                        const double2 ub = updB[i * 32 + lane];
+#pragma unroll
+                        for (int t = 0; t < NCT; t++) {
+                            if (!((tilemask >> t) & 1)) continue;
+                            dmma(q[t][i].x, q[t][i].y, w[t].x, ub.x);
+                            dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
+                        }
                     }
                 }
-                // W^T = Y^T (-T)
-                double2 w[NCT];
+                if (tau + 1 >= NT) { done = true; break; }     // final windows written back below
+                // emit the bottom chunk: to HBM (deepest warp) or to warp d+1 for the next step
+                const int cbot = C0 - tau + d * SPAN + LAM - 1;
+                if (d == D - 1) {
+#pragma unroll
+                    for (int t = 0; t < NCT; t++)
+                        store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
+                    // publish: every chunk >= cbot is final for the next pass
+                    if (j == K - 1 && (st % PUB) == PUB - 1 && cbot <= C0 + 1 && cbot >= 0) {
+                        __threadfence();
+                        __syncwarp();
+                        if (lane == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < NCT; t++) shand[hslot(st & 1, d + 1, j, t)] = q[t][LAM - 1];
+                }
+                // shift the window one chunk; the new top chunk arrived during the previous step
+                if (d == 0 && j == 0) cp_async_wait<1>();
 #pragma unroll
                 for (int t = 0; t < NCT; t++) {
-                    if (!tileok[t]) continue;
-                    double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
-                    if (NACC == 4) {
-                        ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
-                        yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
-                    }
-                    w[t] = make_double2(0.0, 0.0);
-                    dmma(w[t].x, w[t].y, ya, tf.x);
-                    dmma(w[t].x, w[t].y, yb, tf.y);
-                }
-                // Q_W^T += W^T V_g^T
 #pragma unroll
-                for (int i = 0; i < LAM; i++) {
-                    const double2 ub = updB[i * 32 + lane];
-#pragma unroll
-                    for (int t = 0; t < NCT; t++) {
-                        if (!tileok[t]) continue;
-                        dmma(q[t][i].x, q[t][i].y, w[t].x, ub.x);
-                        dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
-                    }
+                    for (int i = LAM - 1; i > 0; i--) q[t][i] = q[t][i - 1];
+                    if (d == 0)
+                        q[t][0] = sintake[islot(st & 1, j, t)];
+                    else if (st > 0)
+                        q[t][0] = shand[hslot((st + 1) & 1, d, j, t)];
+                    else
+                        q[t][0] = make_double2(0.0, 0.0);   // rows below the matrix (chunk >= C0 + 2)
                 }
             }
-            if (st + 1 == nsteps) {       // final windows are written back below
-                if (d == 0) cp_async_wait<0>();   // drain the unused last intake before slot reuse
-                break;
-            }
-            const int64_t cbot = C0 - st + d * LAM + LAM - 1;
-            if (d == D - 1) {
-#pragma unroll
-                for (int t = 0; t < NCT; t++) store_pair(Q, ldq, n, col[t], colok[t], 8 * cbot + rsub, q[t][LAM - 1]);
-                if ((st & 3) == 3 && cbot <= C0 + 1 && cbot >= 0) {
-                    __threadfence();
-                    __syncwarp();
-                    if (lane == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
-                }
-            } else {
-#pragma unroll
-                for (int t = 0; t < NCT; t++)
-                    shand[((((st & 1) * D + d + 1) * CW + cw) * NCT + t) * 32 + lane] = q[t][LAM - 1];
-            }
-            if (d == 0) {
-                if (st + 1 < nsteps) cp_async_wait<1>(); else cp_async_wait<0>();
-            }
+            if (done) break;
             __syncthreads();
-#pragma unroll
-            for (int t = 0; t < NCT; t++) {
-#pragma unroll
-                for (int i = LAM - 1; i > 0; i--) q[t][i] = q[t][i - 1];
-                if (d == 0) {
-                    q[t][0] = sintake[(((st & 1) * CW + cw) * NCT + t) * 32 + lane];
-                } else {
-                    q[t][0] = shand[((((st & 1) * D + d) * CW + cw) * NCT + t) * 32 + lane];
-                }
-            }
         }
-        // write back the final windows (chunks [C0 - nsteps + 1 + d*LAM, ... + LAM))
+        if (d == 0) cp_async_wait<0>();   // drain any unused intake before slot reuse
+        __syncthreads();                  // the last step's hand-off writes are visible below
+        // write back the final windows: top chunk C0 - (NT - 1) + d*SPAN
 #pragma unroll
         for (int t = 0; t < NCT; t++)
 #pragma unroll
             for (int i = 0; i < LAM; i++)
-                store_pair(Q, ldq, n, col[t], colok[t], 8 * (C0 - (nsteps - 1) + d * LAM + i) + rsub, q[t][i]);
+                store_pair(qcol[t], (okmask >> t) & 1, n, 8 * (C0 - (NT - 1) + d * SPAN + i) + rsub, q[t][i]);
+        // chunks in transit between windows (emitted by warp d-1, not yet taken by warp d) are final
+        if (d >= 1) {
+            const int st = (NT - 1) / K;                   // step of the last group-time
+            const int jl = (NT - 1) % K;
+            for (int j = jl; j < K && st > 0; j++) {      // emitted in the previous step
+                const int c = C0 - ((st - 1) * K + j) + (d - 1) * SPAN + LAM - 1;
+#pragma unroll
+                for (int t = 0; t < NCT; t++)
+                    store_pair(qcol[t], (okmask >> t) & 1, n, 8 * c + rsub, shand[hslot((st + 1) & 1, d, j, t)]);
+            }
+            for (int j = 0; j < jl; j++) {                // emitted in this step before the last group-time
+                const int c = C0 - (st * K + j) + (d - 1) * SPAN + LAM - 1;
+#pragma unroll
+                for (int t = 0; t < NCT; t++)
+                    store_pair(qcol[t], (okmask >> t) & 1, n, 8 * c + rsub, shand[hslot(st & 1, d, j, t)]);
+            }
+        }
         __threadfence();
         __syncthreads();  // item complete: publish, and the smem ring/hand-off are free again
         if (threadIdx.x == 0) st_release_u64(prog + k, kPassDone);
-        gstep += nsteps;
+        stage0 = (stage0 + nsteps) % S;
     }
 }
 

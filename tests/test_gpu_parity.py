@@ -59,13 +59,14 @@ def test_reference_kernel_bitwise_real_C1(eb):
 
 
 # ------------------------------------------------------------------ DMMA kernel: tolerance
-SHAPES = [(1, 8, 2), (2, 4, 2), (2, 2, 4), (4, 2, 2), (4, 2, 4), (4, 1, 4), (8, 1, 2), (8, 1, 4), (4, 4, 1), (8, 2, 1)]
+SHAPES = [(1, 2, 4, 1), (1, 2, 4, 2), (2, 2, 4, 1), (2, 2, 4, 2), (2, 2, 4, 4), (4, 2, 4, 1), (4, 2, 4, 2),
+          (4, 1, 4, 2), (8, 1, 4, 1), (2, 4, 2, 1), (2, 4, 2, 2), (2, 2, 3, 1), (2, 2, 3, 2)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("nbw", [8, 16, 32, 64])
 def test_dmma_all_shapes(eb, shape, nbw):
-    D, CW, NCT = shape
+    D, CW, NCT, K = shape
     n, nev = 301, 45                          # ragged: n odd, nev not a multiple of 8
     hv, tau, s, L, Q = synth_case(n, nbw, nev, nbw * 13 + D, ldq=302)
     want = oracle.apply(hv, tau, s, L, Q)
@@ -73,7 +74,7 @@ def test_dmma_all_shapes(eb, shape, nbw):
     # across CTAs through the progress words; 0: all co-resident CTAs
     for grid in (0, 1, 2, 3):
         got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
-                                                         tiles_per_warp=NCT, grid_ctas=grid))
+                                                         tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
         assert _rel(got[:, :n], want[:, :n]) <= TOL, (shape, grid)
         assert np.array_equal(got[:, n:], Q[:, n:])      # ldq padding untouched
 
@@ -127,7 +128,8 @@ def test_column_independence_bitwise(eb):
     for c0, c1 in [(0, 8), (3, 50), (77, 160), (159, 160)]:
         part = run_gpu(eb, n, nbw, hv, tau, Q[c0:c1].copy())
         assert np.array_equal(part, full[c0:c1]), (c0, c1)
-    alt = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=2, depth_warps=8, col_warps=1, tiles_per_warp=2, grid_ctas=5))
+    alt = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=2, depth_warps=8, col_warps=1, tiles_per_warp=4, grid_ctas=5,
+                                                    groups_per_step=1))
     assert np.array_equal(alt, full)
 
 
@@ -176,15 +178,15 @@ def test_full_size_C3_sampled_columns(eb):
     assert _rel(got, want) <= TOL
 
 
-@pytest.mark.parametrize("shape,grid", [((4, 2, 4), 7), ((4, 2, 4), 0), ((1, 8, 2), 5), ((8, 1, 2), 0),
-                                        ((2, 2, 4), 13), ((4, 1, 4), 3)])
+@pytest.mark.parametrize("shape,grid", [((4, 2, 4, 1), 7), ((4, 2, 4, 2), 0), ((1, 2, 4, 2), 5), ((8, 1, 4, 1), 0),
+                                        ((2, 2, 4, 2), 13), ((2, 2, 4, 4), 0), ((4, 1, 4, 2), 3), ((2, 2, 3, 2), 0)])
 def test_multi_item_ctas_at_scale(eb, shape, grid):
     """Many work items per CTA and passes of one tile group running concurrently on
     different CTAs (progress words, slot reuse across items) — the regime of C2/C3."""
-    D, CW, NCT = shape
-    n, nbw, nev = 2000, 32, 520
+    D, CW, NCT, K = shape
+    n, nbw, nev = 2000, 64 if K == 2 else 32, 520
     hv, tau, s, L, Q = synth_case(n, nbw, nev, 31 + D * CW)
     want = oracle.apply(hv, tau, s, L, Q)
     got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
-                                                     tiles_per_warp=NCT, grid_ctas=grid))
+                                                     tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
     assert _rel(got, want) <= TOL

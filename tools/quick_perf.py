@@ -5,7 +5,7 @@ sys.path.insert(0, '.')
 import paper_1811_01277_b200 as eb
 from inputs import synthetic_reflectors, synthetic_q_torch
 
-SHAPES = [(1,8,2), (2,4,2), (2,2,4), (4,2,2), (4,2,4), (4,1,4), (8,1,2), (8,1,4), (4,4,1), (8,2,1)]
+SHAPES = [(1,2,4,1), (1,2,4,2), (2,2,4,1), (2,2,4,2), (2,2,4,4), (4,2,4,1), (4,2,4,2), (4,1,4,2), (8,1,4,1), (2,4,2,1), (2,4,2,2), (2,2,3,1), (2,2,3,2)]
 cfgs = [(20000, 64, 20000), (20000, 64, 2000), (4096, 32, 4096), (20000, 64, 2500), (60000, 64, 3750)]
 if len(sys.argv) > 1:
     cfgs = [tuple(int(v) for v in a.split(',')) for a in sys.argv[1:]]
@@ -20,7 +20,7 @@ for (n, nbw, nev) in cfgs:
     fl = eb.credited_flops(n, nbw, nev)
     for sh in [None] + SHAPES:
         for grid in ([0] if sh is None else [0]):
-            opts = None if sh is None else dict(kernel=2, depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2], grid_ctas=grid)
+            opts = None if sh is None else dict(kernel=2, depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2], grid_ctas=grid, groups_per_step=sh[3])
             try:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 eb.apply_prepared(n, nbw, ws, dq, opts=opts); torch.cuda.synchronize()
