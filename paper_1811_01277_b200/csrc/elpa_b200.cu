@@ -33,7 +33,22 @@ struct Plan {
 int sm_count() {
     int dev = 0, n = kMaxSms;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
     return n > 0 ? n : kMaxSms;
+}
+
+// A failed runtime call leaves a "last error" that a later cudaGetLastError() after a
+// successful launch would report; clear it so every call reports only its own failures.
+int fail_cuda() {
+    cudaGetLastError();
+    return ELPA_B200_ERR_CUDA;
+}
+
+int smem_optin() {
+    int dev = 0, v = 232448;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaGetLastError();   // no device (CPU host): keep the B200 value, clear the error
+    return v > 0 ? v : 232448;
 }
 
 bool b8_supported(int64_t nbw) {
@@ -45,8 +60,10 @@ bool b8_supported(int64_t nbw) {
 // (D, CW, NCT) menu of compiled DMMA configurations
 // (D depth warps, CW column warps, NCT tiles per warp, K groups per step)
 struct Shape { int D, CW, NCT, K; };
-#define ELPA_SHAPES(X) X(1, 2, 4, 1) X(1, 2, 4, 2) X(2, 2, 4, 1) X(2, 2, 4, 2) X(2, 2, 4, 4) X(4, 2, 4, 1) \
-    X(4, 2, 4, 2) X(4, 1, 4, 2) X(8, 1, 4, 1) X(2, 4, 2, 1) X(2, 4, 2, 2) X(2, 2, 3, 1) X(2, 2, 3, 2)
+// K = 1 throughout: measured faster than K = 2/4 at every config (profiles/shape_sweep_r01_k.jsonl);
+// the kernel keeps K as a template parameter for later work.
+#define ELPA_SHAPES(X) X(1, 2, 4, 1) X(2, 2, 4, 1) X(4, 2, 4, 1) X(8, 1, 4, 1) X(2, 4, 2, 1) X(2, 2, 3, 1) \
+    X(2, 2, 2, 1) X(4, 4, 2, 1) X(2, 4, 3, 1)
 #define ELPA_SHAPE_ENTRY(D_, CW_, NCT_, K_) {D_, CW_, NCT_, K_},
 constexpr Shape kShapes[] = {ELPA_SHAPES(ELPA_SHAPE_ENTRY)};
 
@@ -69,8 +86,10 @@ size_t dmma_smem(int b8, int D, int CW, int NCT, int K) {
 // other's per-step barriers.  Work items (tile group, depth pass) are spread dynamically
 // over all SMs, so balance no longer depends on nev / (8 * #SMs).
 void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int &K) {
-    (void)ntile; (void)M; (void)b8;
-    D = 2; CW = 2; NCT = 4; K = 1;
+    (void)ntile; (void)M;
+    K = 1;
+    if (b8 >= 8) { D = 2; CW = 2; NCT = 4; }   // nbw = 64: 24.0 TF/s at C3, 22.1 at C4
+    else { D = 2; CW = 4; NCT = 2; }           // nbw <= 32: 18.9 TF/s at C2
 }
 
 int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
@@ -106,6 +125,7 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     p.grid = p.items;          // capped by co-residency at launch
     p.threads = 32 * D * CW;
     p.smem = dmma_smem(p.b8, D, CW, NCT, K);
+    if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;   // shape does not fit this nbw
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1) * 8 : 0;
     return ELPA_B200_OK;
 }
@@ -144,11 +164,16 @@ template <int B8, int D, int CW, int NCT, int K>
 int64_t dmma_grid(const Plan &p) {
     auto kern = apply_dmma_kernel<B8, D, CW, NCT, K>;
     const size_t smem = DmmaCfg<B8, D, CW, NCT, K>::SMEM;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<B8, D, CW, NCT, K>::THREADS, smem) !=
-            cudaSuccess || per_sm < 1)
+            cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
         return -1;
+    }
     int64_t g = int64_t(per_sm) * sm_count();
     if (p.grid_req > 0 && p.grid_req < g) g = p.grid_req;
     return g < p.items ? g : p.items;
@@ -162,7 +187,7 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     uint64_t *prog = nullptr;
     // one progress word per work item + the work-item counter, zeroed per launch
     const size_t pbytes = size_t(p.items + 1) * 8;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return ELPA_B200_ERR_CUDA;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
     int rc = ELPA_B200_OK;
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
@@ -298,7 +323,7 @@ int elpa_trans_ev_tridi_to_band_ex(int64_t n, int64_t nbw, int64_t nev, const do
     if ((rc = check_device()) != ELPA_B200_OK) return rc;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     void *ws = nullptr;
-    if (p.ws_bytes > 0 && cudaMallocAsync(&ws, size_t(p.ws_bytes), s) != cudaSuccess) return ELPA_B200_ERR_CUDA;
+    if (p.ws_bytes > 0 && cudaMallocAsync(&ws, size_t(p.ws_bytes), s) != cudaSuccess) return fail_cuda();
     rc = prepare_impl(p, n, hh_v, hh_tau, ws, s);
     if (rc == ELPA_B200_OK) rc = apply_impl(p, n, nbw, nev, hh_v, hh_tau, ws, Q, ldq, s);
     if (ws && cudaFreeAsync(ws, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
@@ -326,7 +351,7 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     const size_t off_v = (bq + 255) & ~size_t(255), off_t = off_v + ((bv + 255) & ~size_t(255));
     const size_t off_w = off_t + ((bt + 255) & ~size_t(255));
     if (cudaMallocAsync(reinterpret_cast<void **>(&buf), off_w + size_t(p.ws_bytes), s) != cudaSuccess)
-        return ELPA_B200_ERR_CUDA;
+        return fail_cuda();
     double *dQ = reinterpret_cast<double *>(buf), *dv = reinterpret_cast<double *>(buf + off_v);
     double *dt = reinterpret_cast<double *>(buf + off_t);
     void *ws = p.ws_bytes ? buf + off_w : nullptr;
