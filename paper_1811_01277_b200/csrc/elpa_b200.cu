@@ -63,7 +63,7 @@ struct Shape { int D, CW, NCT, K; };
 // K = 1 throughout: measured faster than K = 2/4 at every config (profiles/shape_sweep_r01_k.jsonl);
 // the kernel keeps K as a template parameter for later work.
 #define ELPA_SHAPES(X) X(1, 2, 4, 1) X(2, 2, 4, 1) X(4, 2, 4, 1) X(8, 1, 4, 1) X(2, 4, 2, 1) X(2, 2, 3, 1) \
-    X(2, 2, 2, 1) X(4, 4, 2, 1) X(2, 4, 3, 1)
+    X(2, 2, 2, 1) X(4, 4, 2, 1) X(2, 4, 3, 1) X(2, 1, 2, 1) X(1, 2, 2, 1) X(4, 2, 2, 1) X(2, 1, 4, 1)
 #define ELPA_SHAPE_ENTRY(D_, CW_, NCT_, K_) {D_, CW_, NCT_, K_},
 constexpr Shape kShapes[] = {ELPA_SHAPES(ELPA_SHAPE_ENTRY)};
 
@@ -80,15 +80,15 @@ size_t dmma_smem(int b8, int D, int CW, int NCT, int K) {
            size_t(2) * K * CW * NCT * 64 * 8 + 64;
 }
 
-// Automatic choice (measured sweep in profiles/shape_sweep_r01.jsonl):
-// D = 2 pipelined depths per work item, 2 column warps x 4 tiles (64 columns per item),
-// 128 threads and ~83 KB shared memory per CTA so two CTAs share an SM and overlap each
+// Automatic choice (measured sweeps in profiles/shape_sweep_r01*.jsonl):
+// D = 2 pipelined depths per work item, 2 column warps x 2 tiles (32 columns per item),
+// 128 threads and ~70 KB shared memory per CTA so three CTAs share an SM and hide each
 // other's per-step barriers.  Work items (tile group, depth pass) are spread dynamically
 // over all SMs, so balance no longer depends on nev / (8 * #SMs).
 void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int &K) {
     (void)ntile; (void)M;
     K = 1;
-    if (b8 >= 8) { D = 2; CW = 2; NCT = 4; }   // nbw = 64: 24.0 TF/s at C3, 22.1 at C4
+    if (b8 >= 8) { D = 2; CW = 2; NCT = 2; }   // nbw = 64: 25.7 TF/s at C3, 24.4 at C4 (3 CTAs/SM)
     else { D = 2; CW = 4; NCT = 2; }           // nbw <= 32: 18.9 TF/s at C2
 }
 
