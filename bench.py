@@ -187,9 +187,11 @@ def main():
     ev_apply = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in range(args.steps)]
 
+    from paper_1811_01277_b200.dist import broadcast_reflectors
+
     def step(i=None):
         if world > 1:
-            dist.broadcast(hh, src=0)
+            broadcast_reflectors(hh, src=0)          # the path's single collective (NCCL)
         eb.prepare(n, nbw, hh_v, hh_tau, ws, stream=stream)
         if i is not None:
             ev_apply[i][0].record(stream)
