@@ -60,7 +60,8 @@ def test_reference_kernel_bitwise_real_C1(eb):
 
 # ------------------------------------------------------------------ DMMA kernel: tolerance
 SHAPES = [(1, 2, 4, 1), (2, 2, 4, 1), (4, 2, 4, 1), (8, 1, 4, 1), (2, 4, 2, 1), (2, 2, 3, 1), (2, 2, 2, 1),
-          (4, 4, 2, 1), (2, 4, 3, 1), (2, 1, 2, 1), (1, 2, 2, 1), (4, 2, 2, 1), (2, 1, 4, 1)]
+          (4, 4, 2, 1), (2, 4, 3, 1), (2, 1, 2, 1), (1, 2, 2, 1), (4, 2, 2, 1), (2, 1, 4, 1), (1, 1, 4, 1),
+          (1, 1, 2, 1), (1, 4, 2, 1), (2, 1, 3, 1)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)

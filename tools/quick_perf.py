@@ -5,7 +5,7 @@ sys.path.insert(0, '.')
 import paper_1811_01277_b200 as eb
 from inputs import synthetic_reflectors, synthetic_q_torch
 
-SHAPES = [(1,2,4,1), (2,2,4,1), (4,2,4,1), (8,1,4,1), (2,4,2,1), (2,2,3,1), (2,2,2,1), (4,4,2,1), (2,4,3,1), (2,1,2,1), (1,2,2,1), (4,2,2,1), (2,1,4,1)]
+SHAPES = [(1,2,4,1), (2,2,4,1), (4,2,4,1), (8,1,4,1), (2,4,2,1), (2,2,3,1), (2,2,2,1), (4,4,2,1), (2,4,3,1), (2,1,2,1), (1,2,2,1), (4,2,2,1), (2,1,4,1), (1,1,4,1), (1,1,2,1), (1,4,2,1), (2,1,3,1)]
 cfgs = [(20000, 64, 20000), (20000, 64, 2000), (4096, 32, 4096), (20000, 64, 2500), (60000, 64, 3750)]
 if len(sys.argv) > 1:
     cfgs = [tuple(int(v) for v in a.split(',')) for a in sys.argv[1:]]
