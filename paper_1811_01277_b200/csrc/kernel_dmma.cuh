@@ -23,6 +23,8 @@
 //   * Prepared fragments of the D groups of the next step are fetched with cp.async.bulk
 //     into a 2-stage shared-memory ring completed on an mbarrier (one elected thread).
 #pragma once
+#include <cstdio>
+
 #include "geometry.cuh"
 
 namespace elpa_b200 {
@@ -45,14 +47,29 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+// Watchdog: a wait that exceeds ~8 s at 1.965 GHz is a protocol bug; report and trap
+// instead of hanging the GPU (the launch then fails with a sticky error).
+constexpr long long kWatchdogCycles = 1ll << 34;
+__device__ __noinline__ void watchdog_fire(const char *what, uint32_t a, uint32_t b) {
+    printf("[elpa_b200 watchdog] block %d thread %d stuck in %s (%u, %u)\n", blockIdx.x, threadIdx.x, what, a, b);
+    __trap();
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity))
+        if (clock64() - t0 > kWatchdogCycles) watchdog_fire("mbarrier", smem_u32(bar), parity);
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile(
@@ -246,9 +263,11 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             if (seen >= need) return;
             if (lane == 0) {
                 uint64_t v = ld_acquire_u64(prog + (k - NX));
+                const long long t0 = clock64();
                 while (v < need) {
                     __nanosleep(128);
                     v = ld_acquire_u64(prog + (k - NX));
+                    if (clock64() - t0 > 4 * kWatchdogCycles) watchdog_fire("progress", uint32_t(k), need);
                 }
                 seen = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(v);
             }
@@ -278,8 +297,10 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             if (threadIdx.x == 0 && st + 1 < NT) issue(st + 1);
             if (d == 0 && st + 1 < NT) intake(st + 1);
             const uint32_t gs = gbase + st, stg = gs % S;
+            // every warp waits for every step's stage, active or not: this bounds each warp to
+            // one step ahead of the producer, so parity waits never alias an older phase
+            mbar_wait(&bfull[stg], (gs / S) & 1u);
             if (group_valid(st, d)) {
-                mbar_wait(&bfull[stg], (gs / S) & 1u);
                 const double2 *dotB = reinterpret_cast<const double2 *>(sblob + (stg * D + d) * BLOB);
                 const double2 *updB = dotB + 32 * LAM;
                 const double2 tf = dotB[64 * LAM + lane];
