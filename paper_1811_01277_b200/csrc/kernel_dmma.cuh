@@ -23,8 +23,6 @@
 //   * Prepared fragments of the D groups of the next step are fetched with cp.async.bulk
 //     into a 2-stage shared-memory ring completed on an mbarrier (one elected thread).
 #pragma once
-#include <cstdio>
-
 #include "geometry.cuh"
 
 namespace elpa_b200 {
@@ -47,13 +45,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Watchdog: a wait that exceeds ~8 s at 1.965 GHz is a protocol bug; report and trap
-// instead of hanging the GPU (the launch then fails with a sticky error).
+// Watchdog: a wait that exceeds ~8 s at 1.965 GHz is a protocol bug; trap instead of hanging
+// the GPU (the launch then fails with a sticky error).  No printf: a call inside the wait loops
+// would force the live register window across an ABI call boundary.
 constexpr long long kWatchdogCycles = 1ll << 34;
-__device__ __noinline__ void watchdog_fire(const char *what, uint32_t a, uint32_t b) {
-    printf("[elpa_b200 watchdog] block %d thread %d stuck in %s (%u, %u)\n", blockIdx.x, threadIdx.x, what, a, b);
-    __trap();
-}
+__device__ __forceinline__ void watchdog_fire(const char *, uint32_t, uint32_t) { asm volatile("trap;"); }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
