@@ -234,7 +234,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             return dd <= dmax && st < NT && g >= 0 && g < G - dd * B8;
         };
         // thread 0: fragments of step st -> stage (gbase + st) % S, after every warp released
-        // that stage's previous use (global step gbase + st - S)
+        // that stage's previous use (global step gbase + st - S); issued S - 1 steps ahead
         auto issue = [&](int st) {
             const uint32_t gs = gbase + st, stg = gs % S;
             if (gs >= S) mbar_wait(&bempty[stg], ((gs / S) - 1) & 1u);
@@ -249,7 +249,8 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                     bulk_g2s(sblob + (stg * D + dd) * BLOB, src, BLOB * 8, &bfull[stg]);
                 }
         };
-        if (threadIdx.x == 0) issue(0);
+        if (threadIdx.x == 0)
+            for (int st = 0; st < S - 1 && st < NT; st++) issue(st);   // prefetch distance S - 1
 
         // cross-pass dependency (depth warp 0 only): chunk c must be final from pass p-1
         uint32_t seen = 0;
@@ -290,7 +291,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         if (d == 0) intake(0);
 
         for (int st = 0;; st++) {
-            if (threadIdx.x == 0 && st + 1 < NT) issue(st + 1);
+            if (threadIdx.x == 0 && st + S - 1 < NT) issue(st + S - 1);
             if (d == 0 && st + 1 < NT) intake(st + 1);
             const uint32_t gs = gbase + st, stg = gs % S;
             // every warp waits for every step's stage, active or not: this bounds each warp to
