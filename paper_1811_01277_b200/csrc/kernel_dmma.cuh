@@ -128,6 +128,12 @@ struct DmmaCfg {
     static constexpr size_t SMEM_HAND = size_t(NPAIR > 0 ? NPAIR : 1) * HS * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM_INTAKE = size_t(2) * CW * NCT * 64 * sizeof(double);
     static constexpr int NBARS = 2 * S + 2 * NPAIR * HS;
+    // CTAs per SM to reserve registers for: the register window (4*LAM*NCT) plus ~80 for
+    // addressing/accumulators; without a bound ptxas spreads to 220+ registers and an SM
+    // holds one CTA fewer (measured: 25.7 -> 19.1 TF/s at C3 for D=2, CW=2, NCT=2).
+    static constexpr int REG_EST = 4 * LAM * NCT + 80;
+    static constexpr int MINB_RAW = 65536 / (THREADS * REG_EST);
+    static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + NBARS * 8 + 16;
 };
 
@@ -150,7 +156,7 @@ constexpr uint64_t kPassDone = ~0ull;
 // ring has full (TMA transaction) and empty (one arrival per warp) mbarriers, and every
 // depth hand-off is a 2-slot ring with full/empty mbarriers, so warps drift independently.
 template <int B8, int D, int CW, int NCT>
-__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT>::THREADS, 1)
+__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT>::THREADS, DmmaCfg<B8, D, CW, NCT>::MINB)
 apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, double *Q, int64_t ldq,
                   uint64_t *prog) {
     using Cfg = DmmaCfg<B8, D, CW, NCT>;
