@@ -58,9 +58,10 @@ bool b8_supported(int64_t nbw) {
 }
 
 // (D, CW, NCT) menu of compiled DMMA configurations
-// (D depth warps, CW column warps, NCT tiles per warp); one reflector group per step
-// (grouping K > 1 per step measured slower at every config: profiles/shape_sweep_r01_k.jsonl)
+// (D depth warps, CW column warps, NCT tiles per warp, K groups per step)
 struct Shape { int D, CW, NCT, K; };
+// K = 1 throughout: measured faster than K = 2/4 at every config (profiles/shape_sweep_r01_k.jsonl);
+// the kernel keeps K as a template parameter for later work.
 #define ELPA_SHAPES(X) X(1, 2, 4, 1) X(2, 2, 4, 1) X(4, 2, 4, 1) X(8, 1, 4, 1) X(2, 4, 2, 1) X(2, 2, 3, 1) \
     X(2, 2, 2, 1) X(4, 4, 2, 1) X(2, 4, 3, 1) X(2, 1, 2, 1) X(1, 2, 2, 1) X(4, 2, 2, 1) X(2, 1, 4, 1) \
     X(1, 1, 4, 1) X(1, 1, 2, 1) X(1, 4, 2, 1) X(2, 1, 3, 1)
@@ -74,12 +75,10 @@ bool shape_compiled(int D, int CW, int NCT, int K) {
 }
 
 size_t dmma_smem(int b8, int D, int CW, int NCT, int K) {
-    (void)K;
     const size_t blob = size_t(128) * (b8 + 1) + 64;
-    const int stages = (D * blob * 8 * 3 <= 120 * 1024) ? 3 : 2;
-    const int npair = (D - 1) * CW;
-    return size_t(stages) * D * blob * 8 + size_t(npair > 0 ? npair : 1) * 2 * NCT * 64 * 8 +
-           size_t(2) * CW * NCT * 64 * 8 + size_t(2 * stages + 4 * npair) * 8 + 16;
+    const int stages = (K * D * blob * 8 * 3 <= 100 * 1024) ? 3 : 2;
+    return size_t(stages) * K * D * blob * 8 + size_t(2) * D * K * CW * NCT * 64 * 8 +
+           size_t(2) * K * CW * NCT * 64 * 8 + 64;
 }
 
 // Automatic choice (measured sweeps in profiles/shape_sweep_r01*.jsonl):
@@ -162,16 +161,16 @@ int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws,
 
 // Grid of the persistent item kernel: the co-resident maximum (more CTAs could not run
 // concurrently anyway; correctness does not depend on co-residency, see kernel_dmma.cuh).
-template <int B8, int D, int CW, int NCT>
+template <int B8, int D, int CW, int NCT, int K>
 int64_t dmma_grid(const Plan &p) {
-    auto kern = apply_dmma_kernel<B8, D, CW, NCT>;
-    const size_t smem = DmmaCfg<B8, D, CW, NCT>::SMEM;
+    auto kern = apply_dmma_kernel<B8, D, CW, NCT, K>;
+    const size_t smem = DmmaCfg<B8, D, CW, NCT, K>::SMEM;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
         cudaGetLastError();
         return -1;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<B8, D, CW, NCT>::THREADS, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<B8, D, CW, NCT, K>::THREADS, smem) !=
             cudaSuccess || per_sm < 1) {
         cudaGetLastError();
         return -1;
@@ -181,10 +180,10 @@ int64_t dmma_grid(const Plan &p) {
     return g < p.items ? g : p.items;
 }
 
-template <int B8, int D, int CW, int NCT>
+template <int B8, int D, int CW, int NCT, int K>
 int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
                       cudaStream_t s) {
-    const int64_t grid = dmma_grid<B8, D, CW, NCT>(p);
+    const int64_t grid = dmma_grid<B8, D, CW, NCT, K>(p);
     if (grid < 1) return ELPA_B200_ERR_CUDA;
     uint64_t *prog = nullptr;
     // one progress word per work item + the work-item counter, zeroed per launch
@@ -193,8 +192,8 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     int rc = ELPA_B200_OK;
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
-        apply_dmma_kernel<B8, D, CW, NCT><<<unsigned(grid), DmmaCfg<B8, D, CW, NCT>::THREADS,
-                                            DmmaCfg<B8, D, CW, NCT>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
+        apply_dmma_kernel<B8, D, CW, NCT, K><<<unsigned(grid), DmmaCfg<B8, D, CW, NCT, K>::THREADS,
+                                               DmmaCfg<B8, D, CW, NCT, K>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     }
     if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
@@ -206,7 +205,7 @@ int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, doub
                    cudaStream_t s) {
 #define ELPA_SHAPE(D_, CW_, NCT_, K_)                          \
     if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
-        return launch_dmma_shape<B8, D_, CW_, NCT_>(p, n, nev, ws, Q, ldq, s);
+        return launch_dmma_shape<B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
     ELPA_SHAPES(ELPA_SHAPE)
 #undef ELPA_SHAPE
     return ELPA_B200_ERR_ARG;

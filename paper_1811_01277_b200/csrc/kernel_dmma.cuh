@@ -42,14 +42,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 // Watchdog: a wait that exceeds ~8 s at 1.965 GHz is a protocol bug; trap instead of hanging
 // the GPU (the launch then fails with a sticky error).  No printf: a call inside the wait loops
 // would force the live register window across an ABI call boundary.
 constexpr long long kWatchdogCycles = 1ll << 34;
-__device__ __forceinline__ void watchdog_fire(const char *, uint32_t, uint32_t) { asm volatile("trap;"); }
+__device__ __forceinline__ void watchdog_fire() { asm volatile("trap;"); }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -65,7 +62,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const long long t0 = clock64();
     while (!mbar_try_wait(bar, parity))
-        if (clock64() - t0 > kWatchdogCycles) watchdog_fire("mbarrier", smem_u32(bar), parity);
+        if (clock64() - t0 > kWatchdogCycles) watchdog_fire();
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile(
@@ -114,27 +111,25 @@ __device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
     asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <int B8, int D, int CW, int NCT>
+template <int B8, int D, int CW, int NCT, int K>
 struct DmmaCfg {
     static constexpr int LAM = B8 + 1;
     static constexpr int BLOB = 128 * LAM + 64;            // doubles per group
     static constexpr int NWARP = D * CW;
     static constexpr int THREADS = 32 * NWARP;
     static constexpr int T = CW * NCT;                     // 8-column tiles per work item
-    static constexpr int S = (D * BLOB * 8 * 3 <= 120 * 1024) ? 3 : 2;   // fragment ring stages
-    static constexpr int HS = 2;                           // hand-off ring slots per warp pair
-    static constexpr int NPAIR = (D - 1) * CW;             // depth hand-off pairs (d -> d+1, cw)
-    static constexpr size_t SMEM_BLOBS = size_t(S) * D * BLOB * sizeof(double);
-    static constexpr size_t SMEM_HAND = size_t(NPAIR > 0 ? NPAIR : 1) * HS * NCT * 64 * sizeof(double);
-    static constexpr size_t SMEM_INTAKE = size_t(2) * CW * NCT * 64 * sizeof(double);
-    static constexpr int NBARS = 2 * S + 2 * NPAIR * HS;
+    static constexpr int STAGES = (K * D * BLOB * 8 * 3 <= 100 * 1024) ? 3 : 2;
+    // shared memory: STAGES x K x D fragment blobs, hand-off chunks [2][D][K][CW][NCT][32],
+    // warp-0 intake chunks [2][K][CW][NCT][32], barriers + the dequeued item index
+    static constexpr size_t SMEM_BLOBS = size_t(STAGES) * K * D * BLOB * sizeof(double);
+    static constexpr size_t SMEM_HAND = size_t(2) * D * K * CW * NCT * 64 * sizeof(double);
+    static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
+    static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
     // CTAs per SM to reserve registers for: the register window (4*LAM*NCT) plus ~80 for
-    // addressing/accumulators; without a bound ptxas spreads to 220+ registers and an SM
-    // holds one CTA fewer (measured: 25.7 -> 19.1 TF/s at C3 for D=2, CW=2, NCT=2).
+    // addressing/accumulators, so ptxas does not spread into registers that cost a CTA/SM
     static constexpr int REG_EST = 4 * LAM * NCT + 80;
     static constexpr int MINB_RAW = 65536 / (THREADS * REG_EST);
     static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
-    static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + NBARS * 8 + 16;
 };
 
 // Progress word of work item (x, p): e means pass p of tile group x has
@@ -149,36 +144,31 @@ constexpr uint64_t kPassDone = ~0ull;
 // Deadlock-free without any co-residency assumption: an item waits only on an item of
 // smaller index, which a running CTA dequeued earlier and finishes by induction.
 //
-// Inside an item, step st: depth warp d applies group g = G - 1 - st + 2d of depth m0 + d; its
-// window's top chunk is C0 - st + d*(LAM + 1).  Depth m0+d+1 trails depth m0+d by two groups,
-// so the chunk warp d takes in after step st is the one warp d-1 emitted after step st - 1
-// (one chunk in transit per warp pair).  There is no CTA-wide barrier per step: the fragment
-// ring has full (TMA transaction) and empty (one arrival per warp) mbarriers, and every
-// depth hand-off is a 2-slot ring with full/empty mbarriers, so warps drift independently.
-template <int B8, int D, int CW, int NCT>
-__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT>::THREADS, DmmaCfg<B8, D, CW, NCT>::MINB)
+// Inside an item, group-time tau = 0, 1, ...: depth warp d applies group
+// g = G - 1 - tau + d*(K+1) of depth m0 + d; its window's top chunk is C0 - tau + d*(LAM + K).
+// Depth m0+d+1 trails depth m0+d by K+1 groups, so the chunk warp d takes in after tau was
+// emitted by warp d-1 after tau - K, i.e. in the previous step: the K chunks between two
+// windows are in transit in shared memory.  One step = K group-times = one CTA barrier.
+template <int B8, int D, int CW, int NCT, int K>
+__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT, K>::THREADS, DmmaCfg<B8, D, CW, NCT, K>::MINB)
 apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, double *Q, int64_t ldq,
                   uint64_t *prog) {
-    using Cfg = DmmaCfg<B8, D, CW, NCT>;
+    using Cfg = DmmaCfg<B8, D, CW, NCT, K>;
     constexpr int LAM = Cfg::LAM;
     constexpr int BLOB = Cfg::BLOB;
-    constexpr int S = Cfg::S;
-    constexpr int HS = Cfg::HS;
+    constexpr int S = Cfg::STAGES;
     constexpr int T = Cfg::T;
     constexpr int B = 8 * B8;
-    constexpr int LAG = 2;                                 // groups depth m+1 trails depth m
-    constexpr int SPAN = LAM + 1;                          // chunk distance between stacked windows
-    constexpr int PUB = 16;                                // publish progress every PUB steps
+    constexpr int LAG = K + 1;                             // groups depth m+1 trails depth m
+    constexpr int SPAN = LAM + K;                          // chunk distance between stacked windows
+    constexpr int PUB = (K >= 4) ? 4 : 16 / K;             // publish progress every PUB steps
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *sblob = reinterpret_cast<double *>(smem_raw);                                        // [S][D][BLOB]
-    double2 *shand = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS);                    // [NPAIR][HS][NCT][32]
-    double2 *sintake = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);  // [2][CW][NCT][32]
-    uint64_t *bfull = reinterpret_cast<uint64_t *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND + Cfg::SMEM_INTAKE);
-    uint64_t *bempty = bfull + S;
-    uint64_t *hfull = bempty + S;                          // [NPAIR][HS]
-    uint64_t *hempty = hfull + Cfg::NPAIR * HS;            // [NPAIR][HS]
-    int *s_item = reinterpret_cast<int *>(bfull + Cfg::NBARS);
+    double *sblob = reinterpret_cast<double *>(smem_raw);                                        // [S][K][D][BLOB]
+    double2 *shand = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS);                    // [2][D][K][CW][NCT][32]
+    double2 *sintake = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);  // [2][K][CW][NCT][32]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND + Cfg::SMEM_INTAKE);
+    int *s_item = reinterpret_cast<int *>(bars + S);
 
     const int n = int(n64), nev = int(nev64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -189,27 +179,20 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
     const int NX = (ntile + T - 1) / T;
     const int NP = (M + D - 1) / D;
     const int rsub = 2 * (lane & 3);
-    const int pair_out = d * CW + cw;                      // this warp -> warp (d+1, cw)
-    const int pair_in = (d - 1) * CW + cw;                 // warp (d-1, cw) -> this warp
-    auto hslot = [&](int pair, int slot, int t) { return ((pair * HS + slot) * NCT + t) * 32 + lane; };
-    auto islot = [&](int par, int t) { return ((par * CW + cw) * NCT + t) * 32 + lane; };
+    // hand-off / intake slot of (parity, j, t) for this lane
+    auto hslot = [&](int par, int dd, int j, int t) {
+        return ((((par * D + dd) * K + j) * CW + cw) * NCT + t) * 32 + lane;
+    };
+    auto islot = [&](int par, int j, int t) { return (((par * K + j) * CW + cw) * NCT + t) * 32 + lane; };
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < S; i++) {
-            mbar_init(&bfull[i], 1);
-            mbar_init(&bempty[i], Cfg::NWARP);
-        }
-        for (int i = 0; i < Cfg::NPAIR * HS; i++) {
-            mbar_init(&hfull[i], 1);
-            mbar_init(&hempty[i], 1);
-        }
+        for (int i = 0; i < S; i++) mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    uint32_t gstep = 0;   // CTA-global step counter: ring stage gstep % S, use gstep / S
-    uint32_t hsent = 0;   // hand-off chunks this warp has sent (d < D-1) ...
-    uint32_t hrecv = 0;   // ... and received (d > 0); both continue across items
+    uint32_t phase_bits = 0;  // parity of the next completion, per stage (all threads track it)
+    int stage0 = 0;           // ring stage of the item's step 0
 
     for (;;) {
         if (threadIdx.x == 0)
@@ -232,33 +215,33 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         }
         const int G = int(groups_at_depth(n64, B8, m0));
         const int dmax = min(D, M - m0) - 1;
-        const int NT = G + dmax * LAG;                     // steps of this item
-        const uint32_t gbase = gstep;
+        const int NT = G + dmax * LAG;                     // group-times of this item
+        const int nsteps = (NT + K - 1) / K;
 
-        auto group_valid = [&](int st, int dd) {
-            const int g = G - 1 - st + dd * LAG;
-            return dd <= dmax && st < NT && g >= 0 && g < G - dd * B8;
+        auto group_valid = [&](int tau, int dd) {
+            const int g = G - 1 - tau + dd * LAG;
+            return dd <= dmax && tau < NT && g >= 0 && g < G - dd * B8;
         };
-        // thread 0: fragments of step st -> stage (gbase + st) % S, after every warp released
-        // that stage's previous use (global step gbase + st - S); issued S - 1 steps ahead
-        auto issue = [&](int st) {
-            const uint32_t gs = gbase + st, stg = gs % S;
-            if (gs >= S) mbar_wait(&bempty[stg], ((gs / S) - 1) & 1u);
+        auto issue = [&](int st) {  // fragments of step st -> ring stage (stage0 + st) % S
+            const int stg = (stage0 + st) % S;
+            uint64_t *bar = &bars[stg];
             uint32_t bytes = 0;
-            for (int dd = 0; dd <= dmax; dd++)
-                if (group_valid(st, dd)) bytes += BLOB * 8;
-            mbar_arrive_expect_tx(&bfull[stg], bytes);
-            for (int dd = 0; dd <= dmax; dd++)
-                if (group_valid(st, dd)) {
-                    const int g = G - 1 - st + dd * LAG;
-                    const double *src = blobs + (group_base(n64, B8, m0 + dd) + g) * BLOB;
-                    bulk_g2s(sblob + (stg * D + dd) * BLOB, src, BLOB * 8, &bfull[stg]);
-                }
+            for (int j = 0; j < K; j++)
+                for (int dd = 0; dd <= dmax; dd++)
+                    if (group_valid(st * K + j, dd)) bytes += BLOB * 8;
+            mbar_arrive_expect_tx(bar, bytes);
+            for (int j = 0; j < K; j++)
+                for (int dd = 0; dd <= dmax; dd++)
+                    if (group_valid(st * K + j, dd)) {
+                        const int g = G - 1 - (st * K + j) + dd * LAG;
+                        const double *src = blobs + (group_base(n64, B8, m0 + dd) + g) * BLOB;
+                        bulk_g2s(sblob + ((stg * K + j) * D + dd) * BLOB, src, BLOB * 8, bar);
+                    }
         };
         if (threadIdx.x == 0)
-            for (int st = 0; st < S - 1 && st < NT; st++) issue(st);   // prefetch distance S - 1
+            for (int st = 0; st < S - 1 && st < nsteps; st++) issue(st);
 
-        // cross-pass dependency (depth warp 0 only): chunk c must be final from pass p-1
+        // cross-pass dependency (warp 0 only): chunk c must be final from pass p-1
         uint32_t seen = 0;
         auto await_chunk = [&](int c) {
             if (p == 0 || c < 0) return;
@@ -270,20 +253,23 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 while (v < need) {
                     __nanosleep(128);
                     v = ld_acquire_u64(prog + (k - NX));
-                    if (clock64() - t0 > 4 * kWatchdogCycles) watchdog_fire("progress", uint32_t(k), need);
+                    if (clock64() - t0 > 4 * kWatchdogCycles) watchdog_fire();
                 }
                 seen = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(v);
             }
             seen = __shfl_sync(0xffffffffu, seen, 0);
         };
-        // depth warp 0 streams its new top chunk HBM -> shared one step ahead (cp.async): the
-        // chunk entering after step st is C0 - st - 1, in slot st & 1
+        // warp 0 streams its new top chunks HBM -> shared (cp.async, one step ahead): the chunk
+        // entering after group-time tau = st*K + j is C0 - tau - 1, in slot [st & 1][j]
         auto intake = [&](int st) {
-            const int c = C0 - st - 1;
-            await_chunk(c);
 #pragma unroll
-            for (int t = 0; t < NCT; t++)
-                load_pair_async(&sintake[islot(st & 1, t)], qcol[t], (okmask >> t) & 1, n, 8 * c + rsub);
+            for (int j = 0; j < K; j++) {
+                const int c = C0 - (st * K + j) - 1;
+                await_chunk(c);
+#pragma unroll
+                for (int t = 0; t < NCT; t++)
+                    load_pair_async(&sintake[islot(st & 1, j, t)], qcol[t], (okmask >> t) & 1, n, 8 * c + rsub);
+            }
             cp_async_commit();
         };
 
@@ -296,135 +282,131 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 q[t][i] = load_pair(qcol[t], (okmask >> t) & 1, n, 8 * (C0 + d * SPAN + i) + rsub);
         if (d == 0) intake(0);
 
-        for (int st = 0;; st++) {
-            if (threadIdx.x == 0 && st + S - 1 < NT) issue(st + S - 1);
-            if (d == 0 && st + 1 < NT) intake(st + 1);
-            const uint32_t gs = gbase + st, stg = gs % S;
-            // every warp waits for every step's stage, active or not: this bounds each warp to
-            // one step ahead of the producer, so parity waits never alias an older phase
-            mbar_wait(&bfull[stg], (gs / S) & 1u);
-            if (group_valid(st, d)) {
-                const double2 *dotB = reinterpret_cast<const double2 *>(sblob + (stg * D + d) * BLOB);
-                const double2 *updB = dotB + 32 * LAM;
-                const double2 tf = dotB[64 * LAM + lane];
-                // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1,
-                // chunk parity) so every warp keeps >= 4 DMMA chains in flight
-                constexpr int NACC = (NCT >= 2) ? 2 : 4;
-                double2 y[NCT][NACC];
+        bool done = false;
+        for (int st = 0; !done; st++) {
+            if (threadIdx.x == 0 && st + S - 1 < nsteps) issue(st + S - 1);
+            if (d == 0 && st + 1 < nsteps) intake(st + 1);
+            const uint32_t stage = uint32_t((stage0 + st) % S);
+            const uint32_t par = (phase_bits >> stage) & 1u;
+            phase_bits ^= (1u << stage);
+            bool waited = false;
+#pragma unroll 1
+            for (int j = 0; j < K; j++) {
+                const int tau = st * K + j;
+                if (group_valid(tau, d)) {
+                    if (!waited) { mbar_wait(&bars[stage], par); waited = true; }
+                    const double2 *dotB = reinterpret_cast<const double2 *>(sblob + ((stage * K + j) * D + d) * BLOB);
+                    const double2 *updB = dotB + 32 * LAM;
+                    const double2 tf = dotB[64 * LAM + lane];
+                    // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1,
+                    // chunk parity) so every warp keeps >= 4 DMMA chains in flight
+                    constexpr int NACC = (NCT >= 2) ? 2 : 4;
+                    double2 y[NCT][NACC];
 #pragma unroll
-                for (int t = 0; t < NCT; t++)
+                    for (int t = 0; t < NCT; t++)
 #pragma unroll
-                    for (int a = 0; a < NACC; a++) y[t][a] = make_double2(0.0, 0.0);
+                        for (int a = 0; a < NACC; a++) y[t][a] = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int i = 0; i < LAM; i++) {
-                    const double2 vb = dotB[i * 32 + lane];
+                    for (int i = 0; i < LAM; i++) {
+                        const double2 vb = dotB[i * 32 + lane];
+#pragma unroll
+                        for (int t = 0; t < NCT; t++) {
+                            if (!((tilemask >> t) & 1)) continue;
+                            double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
+                            double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
+                            dmma(ya.x, ya.y, q[t][i].x, vb.x);
+                            dmma(yb.x, yb.y, q[t][i].y, vb.y);
+                        }
+                    }
+                    // W^T = Y^T (-T)
+                    double2 w[NCT];
 #pragma unroll
                     for (int t = 0; t < NCT; t++) {
                         if (!((tilemask >> t) & 1)) continue;
-                        double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
-                        double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
-                        dmma(ya.x, ya.y, q[t][i].x, vb.x);
-                        dmma(yb.x, yb.y, q[t][i].y, vb.y);
+                        double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
+                        if (NACC == 4) {
+                            ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
+                            yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
+                        }
+                        w[t] = make_double2(0.0, 0.0);
+                        dmma(w[t].x, w[t].y, ya, tf.x);
+                        dmma(w[t].x, w[t].y, yb, tf.y);
+                    }
+                    // Q_W^T += W^T V_g^T
+#pragma unroll
+                    for (int i = 0; i < LAM; i++) {
+                        const double2 ub = updB[i * 32 + lane];
+#pragma unroll
+                        for (int t = 0; t < NCT; t++) {
+                            if (!((tilemask >> t) & 1)) continue;
+                            dmma(q[t][i].x, q[t][i].y, w[t].x, ub.x);
+                            dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
+                        }
                     }
                 }
-                // W^T = Y^T (-T)
-                double2 w[NCT];
+                if (tau + 1 >= NT) { done = true; break; }     // final windows written back below
+                // emit the bottom chunk: to HBM (deepest warp) or to warp d+1 for the next step
+                const int cbot = C0 - tau + d * SPAN + LAM - 1;
+                if (d == D - 1) {
+#pragma unroll
+                    for (int t = 0; t < NCT; t++)
+                        store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
+                    // publish: every chunk >= cbot is final for the next pass
+                    if (j == K - 1 && (st % PUB) == PUB - 1 && cbot <= C0 + 1 && cbot >= 0) {
+                        __threadfence();
+                        __syncwarp();
+                        if (lane == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < NCT; t++) shand[hslot(st & 1, d + 1, j, t)] = q[t][LAM - 1];
+                }
+                // shift the window one chunk; the new top chunk arrived during the previous step
+                if (d == 0 && j == 0) cp_async_wait<1>();
 #pragma unroll
                 for (int t = 0; t < NCT; t++) {
-                    if (!((tilemask >> t) & 1)) continue;
-                    double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
-                    if (NACC == 4) {
-                        ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
-                        yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
-                    }
-                    w[t] = make_double2(0.0, 0.0);
-                    dmma(w[t].x, w[t].y, ya, tf.x);
-                    dmma(w[t].x, w[t].y, yb, tf.y);
-                }
-                // Q_W^T += W^T V_g^T
 #pragma unroll
-                for (int i = 0; i < LAM; i++) {
-                    const double2 ub = updB[i * 32 + lane];
-#pragma unroll
-                    for (int t = 0; t < NCT; t++) {
-                        if (!((tilemask >> t) & 1)) continue;
-                        dmma(q[t][i].x, q[t][i].y, w[t].x, ub.x);
-                        dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
-                    }
+                    for (int i = LAM - 1; i > 0; i--) q[t][i] = q[t][i - 1];
+                    if (d == 0)
+                        q[t][0] = sintake[islot(st & 1, j, t)];
+                    else if (st > 0)
+                        q[t][0] = shand[hslot((st + 1) & 1, d, j, t)];
+                    else
+                        q[t][0] = make_double2(0.0, 0.0);   // rows below the matrix (chunk >= C0 + 2)
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bempty[stg]);      // this warp is done with the stage
-            if (st + 1 >= NT) break;                       // final windows are written back below
-            // emit the bottom chunk: to HBM (deepest warp) or to warp d+1 (it takes it next step)
-            const int cbot = C0 - st + d * SPAN + LAM - 1;
-            if (d == D - 1) {
-#pragma unroll
-                for (int t = 0; t < NCT; t++)
-                    store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
-                // publish: every chunk >= cbot is final for the next pass
-                if ((st % PUB) == PUB - 1 && cbot <= C0 + 1 && cbot >= 0) {
-                    __threadfence();
-                    __syncwarp();
-                    if (lane == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
-                }
-            } else {
-                const uint32_t slot = hsent % HS;
-                if (hsent >= HS) mbar_wait(&hempty[pair_out * HS + slot], ((hsent / HS) - 1) & 1u);
-#pragma unroll
-                for (int t = 0; t < NCT; t++) shand[hslot(pair_out, slot, t)] = q[t][LAM - 1];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&hfull[pair_out * HS + slot]);
-                hsent++;
-            }
-            // shift the window one chunk down and take the new top chunk
-            double2 in[NCT];
-            if (d == 0) {
-                cp_async_wait<1>();
-#pragma unroll
-                for (int t = 0; t < NCT; t++) in[t] = sintake[islot(st & 1, t)];
-            } else if (st == 0) {
-#pragma unroll
-                for (int t = 0; t < NCT; t++) in[t] = make_double2(0.0, 0.0);   // rows below the matrix
-            } else {
-                const uint32_t slot = hrecv % HS;
-                mbar_wait(&hfull[pair_in * HS + slot], (hrecv / HS) & 1u);
-#pragma unroll
-                for (int t = 0; t < NCT; t++) in[t] = shand[hslot(pair_in, slot, t)];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&hempty[pair_in * HS + slot]);
-                hrecv++;
-            }
-#pragma unroll
-            for (int t = 0; t < NCT; t++) {
-#pragma unroll
-                for (int i = LAM - 1; i > 0; i--) q[t][i] = q[t][i - 1];
-                q[t][0] = in[t];
-            }
+            if (done) break;
+            __syncthreads();
         }
-        gstep += NT;
         if (d == 0) cp_async_wait<0>();   // drain any unused intake before slot reuse
+        __syncthreads();                  // the last step's hand-off writes are visible below
         // write back the final windows: top chunk C0 - (NT - 1) + d*SPAN
 #pragma unroll
         for (int t = 0; t < NCT; t++)
 #pragma unroll
             for (int i = 0; i < LAM; i++)
                 store_pair(qcol[t], (okmask >> t) & 1, n, 8 * (C0 - (NT - 1) + d * SPAN + i) + rsub, q[t][i]);
-        // the chunk in transit from warp d-1 (emitted after step NT - 2) is final too
-        if (d >= 1 && NT >= 2) {
-            const uint32_t slot = hrecv % HS;
-            mbar_wait(&hfull[pair_in * HS + slot], (hrecv / HS) & 1u);
-            const int c = C0 - (NT - 2) + (d - 1) * SPAN + LAM - 1;
+        // chunks in transit between windows (emitted by warp d-1, not yet taken by warp d) are final
+        if (d >= 1) {
+            const int st = (NT - 1) / K;                   // step of the last group-time
+            const int jl = (NT - 1) % K;
+            for (int j = jl; j < K && st > 0; j++) {      // emitted in the previous step
+                const int c = C0 - ((st - 1) * K + j) + (d - 1) * SPAN + LAM - 1;
 #pragma unroll
-            for (int t = 0; t < NCT; t++)
-                store_pair(qcol[t], (okmask >> t) & 1, n, 8 * c + rsub, shand[hslot(pair_in, slot, t)]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&hempty[pair_in * HS + slot]);
-            hrecv++;
+                for (int t = 0; t < NCT; t++)
+                    store_pair(qcol[t], (okmask >> t) & 1, n, 8 * c + rsub, shand[hslot((st + 1) & 1, d, j, t)]);
+            }
+            for (int j = 0; j < jl; j++) {                // emitted in this step before the last group-time
+                const int c = C0 - (st * K + j) + (d - 1) * SPAN + LAM - 1;
+#pragma unroll
+                for (int t = 0; t < NCT; t++)
+                    store_pair(qcol[t], (okmask >> t) & 1, n, 8 * c + rsub, shand[hslot(st & 1, d, j, t)]);
+            }
         }
         __threadfence();
-        __syncthreads();  // item complete: publish
+        __syncthreads();  // item complete: publish, and the smem ring/hand-off are free again
         if (threadIdx.x == 0) st_release_u64(prog + k, kPassDone);
+        stage0 = (stage0 + nsteps) % S;
     }
 }
 
