@@ -125,11 +125,6 @@ struct DmmaCfg {
     static constexpr size_t SMEM_HAND = size_t(2) * D * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
-    // CTAs per SM to reserve registers for: the register window (4*LAM*NCT) plus ~80 for
-    // addressing/accumulators, so ptxas does not spread into registers that cost a CTA/SM
-    static constexpr int REG_EST = 4 * LAM * NCT + 80;
-    static constexpr int MINB_RAW = 65536 / (THREADS * REG_EST);
-    static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
 };
 
 // Progress word of work item (x, p): e means pass p of tile group x has
@@ -150,7 +145,7 @@ constexpr uint64_t kPassDone = ~0ull;
 // emitted by warp d-1 after tau - K, i.e. in the previous step: the K chunks between two
 // windows are in transit in shared memory.  One step = K group-times = one CTA barrier.
 template <int B8, int D, int CW, int NCT, int K>
-__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT, K>::THREADS, DmmaCfg<B8, D, CW, NCT, K>::MINB)
+__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT, K>::THREADS, 1)
 apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, double *Q, int64_t ldq,
                   uint64_t *prog) {
     using Cfg = DmmaCfg<B8, D, CW, NCT, K>;

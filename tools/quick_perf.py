@@ -5,7 +5,9 @@ sys.path.insert(0, '.')
 import paper_1811_01277_b200 as eb
 from inputs import synthetic_reflectors, synthetic_q_torch
 
-SHAPES = [(1,2,4,1), (2,2,4,1), (4,2,4,1), (8,1,4,1), (2,4,2,1), (2,2,3,1), (2,2,2,1), (4,4,2,1), (2,4,3,1), (2,1,2,1), (1,2,2,1), (4,2,2,1), (2,1,4,1), (1,1,4,1), (1,1,2,1), (1,4,2,1), (2,1,3,1)]
+import os
+SHAPES = [tuple(int(v) for v in t.split(',')) for t in os.environ['SHAPES'].split()] if os.environ.get('SHAPES') else [(1,2,4,1), (2,2,4,1), (4,2,4,1), (8,1,4,1), (2,4,2,1), (2,2,3,1), (2,2,2,1), (4,4,2,1), (2,4,3,1), (2,1,2,1), (1,2,2,1), (4,2,2,1), (2,1,4,1), (1,1,4,1), (1,1,2,1), (1,4,2,1), (2,1,3,1)]
+REPS = int(os.environ.get('REPS', '2'))
 cfgs = [(20000, 64, 20000), (20000, 64, 2000), (4096, 32, 4096), (20000, 64, 2500), (60000, 64, 3750)]
 if len(sys.argv) > 1:
     cfgs = [tuple(int(v) for v in a.split(',')) for a in sys.argv[1:]]
@@ -25,7 +27,7 @@ for (n, nbw, nev) in cfgs:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 eb.apply_prepared(n, nbw, ws, dq, opts=opts); torch.cuda.synchronize()
                 best = 1e30
-                for _ in range(2):
+                for _ in range(REPS):
                     e0.record(); eb.apply_prepared(n, nbw, ws, dq, opts=opts); e1.record(); torch.cuda.synchronize()
                     best = min(best, e0.elapsed_time(e1))
                 print(json.dumps(dict(n=n, nbw=nbw, nev=nev, shape=sh, grid=grid, ms=round(best, 3), tflops=round(fl / best / 1e9, 3),
