@@ -82,15 +82,15 @@ size_t dmma_smem(int b8, int D, int CW, int NCT, int K) {
 }
 
 // Automatic choice (measured sweeps in profiles/shape_sweep_r01*.jsonl):
-// D = 2 pipelined depths per work item, 2 column warps x 2 tiles (32 columns per item),
-// 128 threads and ~70 KB shared memory per CTA so three CTAs share an SM and hide each
-// other's per-step barriers.  Work items (tile group, depth pass) are spread dynamically
-// over all SMs, so balance no longer depends on nev / (8 * #SMs).
+// small CTAs (64-256 threads, 30-70 KB shared memory) so several share an SM and hide each
+// other's per-step barriers; work items (tile group, depth pass) are spread dynamically over
+// all SMs, so balance no longer depends on nev / (8 * #SMs).
 void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int &K) {
     (void)ntile; (void)M;
     K = 1;
-    if (b8 >= 8) { D = 2; CW = 2; NCT = 2; }   // nbw = 64: 25.7 TF/s at C3, 24.4 at C4 (3 CTAs/SM)
-    else { D = 2; CW = 4; NCT = 2; }           // nbw <= 32: 18.9 TF/s at C2
+    // best of 5 per shape (profiles/shape_sweep_r01_final.jsonl)
+    if (b8 >= 8) { D = 1; CW = 2; NCT = 2; }   // nbw = 64: C3 26.3, C4 24.4, C3/8 shard 24.7 TF/s
+    else { D = 2; CW = 4; NCT = 2; }           // nbw <= 32: C2 18.9 TF/s
 }
 
 int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
