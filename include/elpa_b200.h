@@ -69,8 +69,10 @@ enum {
     ELPA_B200_KERNEL_AUTO = 0,
     ELPA_B200_KERNEL_REFERENCE = 1, /* one thread per column, exact reverse generation order,
                                        no FMA contraction: bitwise equal to the CPU oracle */
-    ELPA_B200_KERNEL_DMMA = 2       /* k = 8 compact-WY groups on FP64 tensor cores (DMMA),
+    ELPA_B200_KERNEL_DMMA = 2,      /* k = 8 compact-WY groups on FP64 tensor cores (DMMA),
                                        depth-pipelined row windows; requires nbw % 8 == 0 */
+    ELPA_B200_KERNEL_DFMA = 3       /* the same groups and schedule on FP64 CUDA cores (DFMA +
+                                       warp shuffles): the measured alternative to DMMA */
 };
 
 /* Optional tuning knobs (the paper's "numerical blocking parameters of the

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libelpa_b200.so")
 
 OK, ERR_ARG, ERR_NULL, ERR_ALIGN, ERR_DEVICE, ERR_CUDA, ERR_SPACE = 0, -1, -2, -3, -4, -5, -6
-KERNEL_AUTO, KERNEL_REFERENCE, KERNEL_DMMA = 0, 1, 2
+KERNEL_AUTO, KERNEL_REFERENCE, KERNEL_DMMA, KERNEL_DFMA = 0, 1, 2, 3
 
 
 def _load():

@@ -68,14 +68,23 @@ struct Shape { int D, CW, NCT, K; };
 #define ELPA_SHAPE_ENTRY(D_, CW_, NCT_, K_) {D_, CW_, NCT_, K_},
 constexpr Shape kShapes[] = {ELPA_SHAPES(ELPA_SHAPE_ENTRY)};
 
-bool shape_compiled(int D, int CW, int NCT, int K) {
+// the DFMA comparison kernel is compiled for a smaller menu
+#define ELPA_DFMA_SHAPES(X) X(1, 2, 2, 1) X(2, 2, 2, 1) X(1, 4, 2, 1) X(2, 4, 2, 1) X(1, 2, 4, 1) X(2, 2, 4, 1)
+constexpr Shape kDfmaShapes[] = {ELPA_DFMA_SHAPES(ELPA_SHAPE_ENTRY)};
+
+bool shape_compiled(bool dfma, int D, int CW, int NCT, int K) {
+    if (dfma) {
+        for (const Shape &s : kDfmaShapes)
+            if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
+        return false;
+    }
     for (const Shape &s : kShapes)
         if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
     return false;
 }
 
-size_t dmma_smem(int b8, int D, int CW, int NCT, int K) {
-    const size_t blob = size_t(128) * (b8 + 1) + 64;
+size_t dmma_smem(int b8, int D, int CW, int NCT, int K, int kind) {
+    const size_t blob = size_t(blob_doubles(b8 + 1, kind));
     const int stages = (K * D * blob * 8 * 3 <= 100 * 1024) ? 3 : 2;
     return size_t(stages) * K * D * blob * 8 + size_t(2) * D * K * CW * NCT * 64 * 8 +
            size_t(2) * K * CW * NCT * 64 * 8 + 64;
@@ -95,10 +104,11 @@ void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int
 
 int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
     int kernel = o ? o->kernel : ELPA_B200_KERNEL_AUTO;
-    if (kernel < ELPA_B200_KERNEL_AUTO || kernel > ELPA_B200_KERNEL_DMMA) return ELPA_B200_ERR_ARG;
+    if (kernel < ELPA_B200_KERNEL_AUTO || kernel > ELPA_B200_KERNEL_DFMA) return ELPA_B200_ERR_ARG;
     if (kernel == ELPA_B200_KERNEL_AUTO)
         kernel = b8_supported(nbw) ? ELPA_B200_KERNEL_DMMA : ELPA_B200_KERNEL_REFERENCE;
-    if (kernel == ELPA_B200_KERNEL_DMMA && !b8_supported(nbw)) return ELPA_B200_ERR_ARG;
+    if ((kernel == ELPA_B200_KERNEL_DMMA || kernel == ELPA_B200_KERNEL_DFMA) && !b8_supported(nbw))
+        return ELPA_B200_ERR_ARG;
     p.kernel = kernel;
     if (kernel == ELPA_B200_KERNEL_REFERENCE) {
         p.threads = 128;
@@ -114,10 +124,11 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     if (D == 0 && CW == 0 && NCT == 0) {
         int Ka = 0;
         auto_shape(ntile, M, p.b8, D, CW, NCT, Ka);
+        if (kernel == ELPA_B200_KERNEL_DFMA) { D = 1; CW = 2; NCT = 2; }   // in the DFMA menu
         if (K == 0) K = Ka;
     }
     if (K == 0) K = 1;
-    if (!shape_compiled(D, CW, NCT, K)) return ELPA_B200_ERR_ARG;
+    if (!shape_compiled(kernel == ELPA_B200_KERNEL_DFMA, D, CW, NCT, K)) return ELPA_B200_ERR_ARG;
     p.D = D; p.CW = CW; p.NCT = NCT; p.K = K;
     p.grid_req = o ? o->grid_ctas : 0;
     if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
@@ -125,9 +136,9 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     p.items = p.nx * ((M + D - 1) / D);
     p.grid = p.items;          // capped by co-residency at launch
     p.threads = 32 * D * CW;
-    p.smem = dmma_smem(p.b8, D, CW, NCT, K);
+    p.smem = dmma_smem(p.b8, D, CW, NCT, K, kernel == ELPA_B200_KERNEL_DFMA);
     if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;   // shape does not fit this nbw
-    p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1) * 8 : 0;
+    p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1, kernel == ELPA_B200_KERNEL_DFMA) * 8 : 0;
     return ELPA_B200_OK;
 }
 
@@ -151,26 +162,27 @@ int validate(int64_t n, int64_t nbw, int64_t nev, const void *hh_v, const void *
 }
 
 template <int B8>
-int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws, cudaStream_t s) {
+int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws, int kind, cudaStream_t s) {
     const int64_t M = num_depths(n, 8 * B8);
     const int64_t G0 = groups_at_depth(n, B8, 0);
     dim3 grid(unsigned((G0 + 3) / 4), unsigned(M));
-    prep_dmma_kernel<B8><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
+    if (kind == 1) prep_dmma_kernel<B8, 1><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
+    else prep_dmma_kernel<B8, 0><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
 }
 
 // Grid of the persistent item kernel: the co-resident maximum (more CTAs could not run
 // concurrently anyway; correctness does not depend on co-residency, see kernel_dmma.cuh).
-template <int B8, int D, int CW, int NCT, int K>
+template <int KIND, int B8, int D, int CW, int NCT, int K>
 int64_t dmma_grid(const Plan &p) {
-    auto kern = apply_dmma_kernel<B8, D, CW, NCT, K>;
-    const size_t smem = DmmaCfg<B8, D, CW, NCT, K>::SMEM;
+    auto kern = apply_dmma_kernel<KIND, B8, D, CW, NCT, K>;
+    const size_t smem = DmmaCfg<KIND, B8, D, CW, NCT, K>::SMEM;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
         cudaGetLastError();
         return -1;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<B8, D, CW, NCT, K>::THREADS, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DmmaCfg<KIND, B8, D, CW, NCT, K>::THREADS, smem) !=
             cudaSuccess || per_sm < 1) {
         cudaGetLastError();
         return -1;
@@ -180,10 +192,10 @@ int64_t dmma_grid(const Plan &p) {
     return g < p.items ? g : p.items;
 }
 
-template <int B8, int D, int CW, int NCT, int K>
+template <int KIND, int B8, int D, int CW, int NCT, int K>
 int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
                       cudaStream_t s) {
-    const int64_t grid = dmma_grid<B8, D, CW, NCT, K>(p);
+    const int64_t grid = dmma_grid<KIND, B8, D, CW, NCT, K>(p);
     if (grid < 1) return ELPA_B200_ERR_CUDA;
     uint64_t *prog = nullptr;
     // one progress word per work item + the work-item counter, zeroed per launch
@@ -192,8 +204,8 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     int rc = ELPA_B200_OK;
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
-        apply_dmma_kernel<B8, D, CW, NCT, K><<<unsigned(grid), DmmaCfg<B8, D, CW, NCT, K>::THREADS,
-                                               DmmaCfg<B8, D, CW, NCT, K>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
+        apply_dmma_kernel<KIND, B8, D, CW, NCT, K><<<unsigned(grid), DmmaCfg<KIND, B8, D, CW, NCT, K>::THREADS,
+                                                     DmmaCfg<KIND, B8, D, CW, NCT, K>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     }
     if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
@@ -205,20 +217,29 @@ int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, doub
                    cudaStream_t s) {
 #define ELPA_SHAPE(D_, CW_, NCT_, K_)                          \
     if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
-        return launch_dmma_shape<B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
-    ELPA_SHAPES(ELPA_SHAPE)
+        return launch_dmma_shape<KIND_DMMA, B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
+#define ELPA_DFMA_SHAPE(D_, CW_, NCT_, K_)                     \
+    if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
+        return launch_dmma_shape<KIND_DFMA, B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
+    if (p.kernel == ELPA_B200_KERNEL_DFMA) {
+        ELPA_DFMA_SHAPES(ELPA_DFMA_SHAPE)
+    } else {
+        ELPA_SHAPES(ELPA_SHAPE)
+    }
 #undef ELPA_SHAPE
+#undef ELPA_DFMA_SHAPE
     return ELPA_B200_ERR_ARG;
 }
 
 int prepare_impl(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, void *ws, cudaStream_t s) {
-    if (p.kernel != ELPA_B200_KERNEL_DMMA || p.ws_bytes == 0) return ELPA_B200_OK;
+    if (p.kernel == ELPA_B200_KERNEL_REFERENCE || p.ws_bytes == 0) return ELPA_B200_OK;
     double *w = static_cast<double *>(ws);
+    const int kind = p.kernel == ELPA_B200_KERNEL_DFMA ? 1 : 0;
     switch (p.b8) {
-        case 1: return launch_prep<1>(n, hh_v, hh_tau, w, s);
-        case 2: return launch_prep<2>(n, hh_v, hh_tau, w, s);
-        case 4: return launch_prep<4>(n, hh_v, hh_tau, w, s);
-        case 8: return launch_prep<8>(n, hh_v, hh_tau, w, s);
+        case 1: return launch_prep<1>(n, hh_v, hh_tau, w, kind, s);
+        case 2: return launch_prep<2>(n, hh_v, hh_tau, w, kind, s);
+        case 4: return launch_prep<4>(n, hh_v, hh_tau, w, kind, s);
+        case 8: return launch_prep<8>(n, hh_v, hh_tau, w, kind, s);
     }
     return ELPA_B200_ERR_ARG;
 }
@@ -275,10 +296,11 @@ int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts
     if (rc != ELPA_B200_OK) return rc;
     if (buf && buflen)
         snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NCT=%d K=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
-                 p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : "reference", p.b8, p.D, p.CW, p.NCT, p.K, (long long)p.items,
+                 p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : (p.kernel == ELPA_B200_KERNEL_DFMA ? "dfma" : "reference"),
+                 p.b8, p.D, p.CW, p.NCT, p.K, (long long)p.items,
                  p.grid_req, p.threads, p.smem, (long long)p.ws_bytes);
     if (hh_total(n, nbw) == 0 || nev == 0) return 0;
-    return p.kernel == ELPA_B200_KERNEL_DMMA ? 2 : 1;
+    return p.kernel == ELPA_B200_KERNEL_REFERENCE ? 1 : 2;
 }
 
 int elpa_b200_prepare(int64_t n, int64_t nbw, const double *hh_v, const double *hh_tau, void *workspace,
@@ -305,7 +327,7 @@ int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev, const double *
     if ((rc = make_plan(n, nbw, nev, opts, p)) != ELPA_B200_OK) return rc;
     if (hh_total(n, nbw) == 0 || nev == 0) return ELPA_B200_OK;
     if (p.kernel == ELPA_B200_KERNEL_REFERENCE && (!hh_v || !hh_tau)) return ELPA_B200_ERR_NULL;
-    if (p.kernel == ELPA_B200_KERNEL_DMMA) {
+    if (p.kernel != ELPA_B200_KERNEL_REFERENCE) {
         if (!workspace) return ELPA_B200_ERR_NULL;
         if (reinterpret_cast<uintptr_t>(workspace) & 255) return ELPA_B200_ERR_ALIGN;
         if (workspace_bytes < size_t(p.ws_bytes)) return ELPA_B200_ERR_SPACE;

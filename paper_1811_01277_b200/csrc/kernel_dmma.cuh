@@ -23,6 +23,8 @@
 //   * Prepared fragments of the D groups of the next step are fetched with cp.async.bulk
 //     into a 2-stage shared-memory ring completed on an mbarrier (one elected thread).
 #pragma once
+#include <type_traits>
+
 #include "geometry.cuh"
 
 namespace elpa_b200 {
@@ -111,10 +113,160 @@ __device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
     asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <int B8, int D, int CW, int NCT, int K>
+// ---------------------------------------------------------------------------------------
+// Per-group arithmetic for one warp: its NCT 8-column tiles, window
+// q[t][i] in the m8n8k4 accumulator layout (lane l: rows 8i + 2(l%4) + {0,1} of column l/4).
+// Two policies compute the same compact-WY group, Q_W <- Q_W - V_g T^T V_g^T Q_W:
+// ---------------------------------------------------------------------------------------
+enum { KIND_DMMA = 0, KIND_DFMA = 1 };
+
+// FP64 tensor cores: 2*LAM + 2 + 2*LAM DMMA.8x8x4 per tile, no shuffles.  Blob layout
+// (prep kernel): dot B-fragments [LAM][32 lanes][2], update B-fragments [LAM][32][2] (== V
+// row-major 8 x 8 per chunk), -T fragments [32][2].
+template <int LAM, int NCT>
+struct DmmaGroup {
+    static constexpr int BLOB = 128 * LAM + 64;
+    __device__ __forceinline__ static void apply(double2 (&q)[NCT][LAM], const double *blob, uint32_t tilemask,
+                                                 int lane) {
+        const double2 *dotB = reinterpret_cast<const double2 *>(blob);
+        const double2 *updB = dotB + 32 * LAM;
+        const double2 tf = dotB[64 * LAM + lane];
+        // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1, chunk
+        // parity) so every warp keeps >= 4 DMMA chains in flight
+        constexpr int NACC = (NCT >= 2) ? 2 : 4;
+        double2 y[NCT][NACC];
+#pragma unroll
+        for (int t = 0; t < NCT; t++)
+#pragma unroll
+            for (int a = 0; a < NACC; a++) y[t][a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < LAM; i++) {
+            const double2 vb = dotB[i * 32 + lane];
+#pragma unroll
+            for (int t = 0; t < NCT; t++) {
+                if (!((tilemask >> t) & 1)) continue;
+                double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
+                double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
+                dmma(ya.x, ya.y, q[t][i].x, vb.x);
+                dmma(yb.x, yb.y, q[t][i].y, vb.y);
+            }
+        }
+        // W^T = Y^T (-T)
+        double2 w[NCT];
+#pragma unroll
+        for (int t = 0; t < NCT; t++) {
+            if (!((tilemask >> t) & 1)) continue;
+            double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
+            if (NACC == 4) {
+                ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
+                yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
+            }
+            w[t] = make_double2(0.0, 0.0);
+            dmma(w[t].x, w[t].y, ya, tf.x);
+            dmma(w[t].x, w[t].y, yb, tf.y);
+        }
+        // Q_W^T += W^T V_g^T
+#pragma unroll
+        for (int i = 0; i < LAM; i++) {
+            const double2 ub = updB[i * 32 + lane];
+#pragma unroll
+            for (int t = 0; t < NCT; t++) {
+                if (!((tilemask >> t) & 1)) continue;
+                dmma(q[t][i].x, q[t][i].y, w[t].x, ub.x);
+                dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
+            }
+        }
+    }
+};
+
+// FP64 CUDA cores (DFMA): lane l holds rows 2(l%4)+{0,1} of every chunk of column l/4, forms
+// partial V^T q over its rows, reduces over the 4 lanes of the column with 2 butterfly
+// shuffles, applies -T^T redundantly per lane, then updates its rows.  Same flops as the DMMA
+// policy (+ the triangular T step), but 32-lane FMAs instead of 8x8x4 tiles.  Blob layout:
+// V row-major [8*LAM rows][VST = 10] (padding makes the 4 row-groups of a warp hit distinct
+// bank groups), then M = -T^T row-major [8][8].
+template <int LAM, int NCT>
+struct DfmaGroup {
+    static constexpr int VST = 10;
+    static constexpr int BLOB = 8 * LAM * VST + 64;
+    __device__ __forceinline__ static void apply(double2 (&q)[NCT][LAM], const double *blob, uint32_t tilemask,
+                                                 int lane) {
+        const int rho = lane & 3;
+        double y[NCT][8];
+#pragma unroll
+        for (int t = 0; t < NCT; t++)
+#pragma unroll
+            for (int a = 0; a < 8; a++) y[t][a] = 0.0;
+#pragma unroll
+        for (int i = 0; i < LAM; i++)
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const double2 *vr = reinterpret_cast<const double2 *>(blob + (8 * i + 2 * rho + r) * VST);
+                double v[8];
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    const double2 vv = vr[m];
+                    v[2 * m] = vv.x;
+                    v[2 * m + 1] = vv.y;
+                }
+#pragma unroll
+                for (int t = 0; t < NCT; t++) {
+                    if (!((tilemask >> t) & 1)) continue;
+                    const double qq = r ? q[t][i].y : q[t][i].x;
+#pragma unroll
+                    for (int a = 0; a < 8; a++) y[t][a] = fma(v[a], qq, y[t][a]);
+                }
+                asm volatile("" ::: "memory");   // keep each row's V loads next to their FMAs
+            }
+#pragma unroll
+        for (int t = 0; t < NCT; t++)
+#pragma unroll
+            for (int a = 0; a < 8; a++) {
+                y[t][a] += __shfl_xor_sync(0xffffffffu, y[t][a], 1);
+                y[t][a] += __shfl_xor_sync(0xffffffffu, y[t][a], 2);
+            }
+        const double *M = blob + 8 * LAM * VST;        // M[a][a'] = -T[a'][a], zero for a' > a
+        double w[NCT][8];
+#pragma unroll
+        for (int a = 0; a < 8; a++) {
+#pragma unroll
+            for (int t = 0; t < NCT; t++) w[t][a] = 0.0;
+#pragma unroll
+            for (int b = 0; b <= a; b++) {
+                const double mab = M[8 * a + b];
+#pragma unroll
+                for (int t = 0; t < NCT; t++) w[t][a] = fma(mab, y[t][b], w[t][a]);
+            }
+        }
+#pragma unroll
+        // Q_W += V_g W', reflector pairs outermost: each element still sums a = 0..7 in order,
+        // but the 2*LAM rows give independent chains without keeping every row's V live
+        for (int ap = 0; ap < 4; ap++)
+#pragma unroll
+            for (int i = 0; i < LAM; i++)
+#pragma unroll
+                for (int r = 0; r < 2; r++) {
+                    const double2 vv = reinterpret_cast<const double2 *>(blob + (8 * i + 2 * rho + r) * VST)[ap];
+#pragma unroll
+                    for (int t = 0; t < NCT; t++) {
+                        if (!((tilemask >> t) & 1)) continue;
+                        double acc = r ? q[t][i].y : q[t][i].x;
+                        acc = fma(vv.x, w[t][2 * ap], acc);
+                        acc = fma(vv.y, w[t][2 * ap + 1], acc);
+                        if (r) q[t][i].y = acc; else q[t][i].x = acc;
+                    }
+                }
+    }
+};
+
+template <int KIND, int LAM, int NCT>
+using GroupOf = typename std::conditional<KIND == KIND_DMMA, DmmaGroup<LAM, NCT>, DfmaGroup<LAM, NCT>>::type;
+
+template <int KIND, int B8, int D, int CW, int NCT, int K>
 struct DmmaCfg {
     static constexpr int LAM = B8 + 1;
-    static constexpr int BLOB = 128 * LAM + 64;            // doubles per group
+    using Group = GroupOf<KIND, LAM, NCT>;
+    static constexpr int BLOB = Group::BLOB;               // doubles per prepared group
     static constexpr int NWARP = D * CW;
     static constexpr int THREADS = 32 * NWARP;
     static constexpr int T = CW * NCT;                     // 8-column tiles per work item
@@ -125,6 +277,10 @@ struct DmmaCfg {
     static constexpr size_t SMEM_HAND = size_t(2) * D * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
+    // DFMA policy: cap registers near 168 (unbounded, ptxas hoists every shared V load of a
+    // group and spills ~1 KB); the DMMA policy needs no bound
+    static constexpr int MINB_DFMA = 65536 / (THREADS * 168);
+    static constexpr int MINB = (KIND == KIND_DFMA && MINB_DFMA > 1) ? MINB_DFMA : 1;
 };
 
 // Progress word of work item (x, p): e means pass p of tile group x has
@@ -144,11 +300,11 @@ constexpr uint64_t kPassDone = ~0ull;
 // Depth m0+d+1 trails depth m0+d by K+1 groups, so the chunk warp d takes in after tau was
 // emitted by warp d-1 after tau - K, i.e. in the previous step: the K chunks between two
 // windows are in transit in shared memory.  One step = K group-times = one CTA barrier.
-template <int B8, int D, int CW, int NCT, int K>
-__global__ void __launch_bounds__(DmmaCfg<B8, D, CW, NCT, K>::THREADS, 1)
+template <int KIND, int B8, int D, int CW, int NCT, int K>
+__global__ void __launch_bounds__(DmmaCfg<KIND, B8, D, CW, NCT, K>::THREADS, DmmaCfg<KIND, B8, D, CW, NCT, K>::MINB)
 apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, double *Q, int64_t ldq,
                   uint64_t *prog) {
-    using Cfg = DmmaCfg<B8, D, CW, NCT, K>;
+    using Cfg = DmmaCfg<KIND, B8, D, CW, NCT, K>;
     constexpr int LAM = Cfg::LAM;
     constexpr int BLOB = Cfg::BLOB;
     constexpr int S = Cfg::STAGES;
@@ -290,54 +446,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 const int tau = st * K + j;
                 if (group_valid(tau, d)) {
                     if (!waited) { mbar_wait(&bars[stage], par); waited = true; }
-                    const double2 *dotB = reinterpret_cast<const double2 *>(sblob + ((stage * K + j) * D + d) * BLOB);
-                    const double2 *updB = dotB + 32 * LAM;
-                    const double2 tf = dotB[64 * LAM + lane];
-                    // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1,
-                    // chunk parity) so every warp keeps >= 4 DMMA chains in flight
-                    constexpr int NACC = (NCT >= 2) ? 2 : 4;
-                    double2 y[NCT][NACC];
-#pragma unroll
-                    for (int t = 0; t < NCT; t++)
-#pragma unroll
-                        for (int a = 0; a < NACC; a++) y[t][a] = make_double2(0.0, 0.0);
-#pragma unroll
-                    for (int i = 0; i < LAM; i++) {
-                        const double2 vb = dotB[i * 32 + lane];
-#pragma unroll
-                        for (int t = 0; t < NCT; t++) {
-                            if (!((tilemask >> t) & 1)) continue;
-                            double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
-                            double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
-                            dmma(ya.x, ya.y, q[t][i].x, vb.x);
-                            dmma(yb.x, yb.y, q[t][i].y, vb.y);
-                        }
-                    }
-                    // W^T = Y^T (-T)
-                    double2 w[NCT];
-#pragma unroll
-                    for (int t = 0; t < NCT; t++) {
-                        if (!((tilemask >> t) & 1)) continue;
-                        double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
-                        if (NACC == 4) {
-                            ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
-                            yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
-                        }
-                        w[t] = make_double2(0.0, 0.0);
-                        dmma(w[t].x, w[t].y, ya, tf.x);
-                        dmma(w[t].x, w[t].y, yb, tf.y);
-                    }
-                    // Q_W^T += W^T V_g^T
-#pragma unroll
-                    for (int i = 0; i < LAM; i++) {
-                        const double2 ub = updB[i * 32 + lane];
-#pragma unroll
-                        for (int t = 0; t < NCT; t++) {
-                            if (!((tilemask >> t) & 1)) continue;
-                            dmma(q[t][i].x, q[t][i].y, w[t].x, ub.x);
-                            dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
-                        }
-                    }
+                    Cfg::Group::apply(q, sblob + ((stage * K + j) * D + d) * BLOB, tilemask, lane);
                 }
                 if (tau + 1 >= NT) { done = true; break; }     // final windows written back below
                 // emit the bottom chunk: to HBM (deepest warp) or to warp d+1 for the next step

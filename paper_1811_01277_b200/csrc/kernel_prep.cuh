@@ -10,12 +10,13 @@
 //   updB[i][lane] = (V[8i + lane/4][2(lane%4)],  V[8i + lane/4][2(lane%4) + 1])
 //   tf[lane]      = (-T[2(lane%4)][lane/4],      -T[2(lane%4) + 1][lane/4])
 // One warp per group.  Missing reflectors (j < 0 or j > J_m) get tau = 0 (identity).
+// KIND 1 (DFMA kernel) instead writes V row-major with row stride 10 and M = -T^T row-major.
 #pragma once
 #include "geometry.cuh"
 
 namespace elpa_b200 {
 
-template <int B8>
+template <int B8, int KIND>
 __global__ void __launch_bounds__(128)
 prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__restrict__ hh_tau,
                  double *__restrict__ blobs) {
@@ -69,7 +70,15 @@ prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__res
         if (lane == a) Ts[warp][a][a] = ta;
         __syncwarp();
     }
-    double *blob = blobs + (group_base(n, B8, m) + g) * blob_doubles(LAM);
+    double *blob = blobs + (group_base(n, B8, m) + g) * blob_doubles(LAM, KIND);
+    if (KIND == 1) {
+        for (int idx = lane; idx < WR * 10; idx += 32) {
+            const int w = idx / 10, a = idx % 10;
+            blob[idx] = (a < 8) ? V[w][a] : 0.0;
+        }
+        for (int e = lane; e < 64; e += 32) blob[WR * 10 + e] = -Ts[warp][e & 7][e >> 3];
+        return;
+    }
     const int kq = lane & 3, gq = lane >> 2;
     for (int i = 0; i < LAM; i++) {
         double2 d, u;

@@ -205,3 +205,28 @@ def test_multi_item_ctas_at_scale(eb, shape, grid):
     got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
                                                      tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
     assert _rel(got, want) <= TOL
+
+
+DFMA_SHAPES = [(1, 2, 2, 1), (2, 2, 2, 1), (1, 4, 2, 1), (2, 4, 2, 1), (1, 2, 4, 1), (2, 2, 4, 1)]
+
+
+@pytest.mark.parametrize("shape", DFMA_SHAPES)
+@pytest.mark.parametrize("nbw", [8, 32, 64])
+def test_dfma_kernel_shapes(eb, shape, nbw):
+    """The DFMA comparison kernel (same groups, schedule and items on CUDA cores)."""
+    D, CW, NCT, K = shape
+    n, nev = 301, 45
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, nbw * 7 + D, ldq=302)
+    want = oracle.apply(hv, tau, s, L, Q)
+    for grid in (0, 2):
+        got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DFMA, depth_warps=D, col_warps=CW,
+                                                         tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
+        assert _rel(got[:, :n], want[:, :n]) <= TOL, (shape, grid)
+        assert np.array_equal(got[:, n:], Q[:, n:])
+
+
+def test_dfma_real_C1_residual(eb):
+    case = oracle.make_case(512, 16, 512, config_seed(1))
+    got = run_gpu(eb, 512, 16, case["hh_v"], case["hh_tau"], case["Qin"], opts=dict(kernel=eb.KERNEL_DFMA))
+    assert _rel(got, case["Qref"]) <= TOL
+    assert oracle.residual(case["band"], got, case["lam"]) <= 1e-13

@@ -22,7 +22,7 @@ for (n, nbw, nev) in cfgs:
     fl = eb.credited_flops(n, nbw, nev)
     for sh in [None] + SHAPES:
         for grid in ([0] if sh is None else [0]):
-            opts = None if sh is None else dict(kernel=2, depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2], grid_ctas=grid, groups_per_step=sh[3])
+            opts = None if sh is None else dict(kernel=int(os.environ.get('KERNEL', '2')), depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2], grid_ctas=grid, groups_per_step=sh[3])
             try:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 eb.apply_prepared(n, nbw, ws, dq, opts=opts); torch.cuda.synchronize()
