@@ -373,6 +373,18 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     char *buf = nullptr;
     const size_t off_v = (bq + 255) & ~size_t(255), off_t = off_v + ((bv + 255) & ~size_t(255));
     const size_t off_w = off_t + ((bt + 255) & ~size_t(255));
+    // Keep the transient buffers cached in the device's default pool between calls: with the
+    // default release threshold (0) every synchronising call would unmap and remap ~GBs.
+    {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 0, want = uint64_t(off_w + size_t(p.ws_bytes));
+            if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess && thr < want)
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
+        }
+        cudaGetLastError();
+    }
     if (cudaMallocAsync(reinterpret_cast<void **>(&buf), off_w + size_t(p.ws_bytes), s) != cudaSuccess)
         return fail_cuda();
     double *dQ = reinterpret_cast<double *>(buf), *dv = reinterpret_cast<double *>(buf + off_v);
