@@ -3,8 +3,10 @@
 // Build: see paper_1811_01277_b200/build.py (nvcc -gencode arch=compute_100a,code=sm_100a).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "../../include/elpa_b200.h"
 #include "geometry.cuh"
@@ -369,37 +371,90 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     if (R == 0 || nev == 0) return ELPA_B200_OK;
     if ((rc = check_device()) != ELPA_B200_OK) return rc;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const size_t bq = size_t(ldq) * nev * 8, bv = size_t(R) * nbw * 8, bt = size_t(R) * 8;
-    char *buf = nullptr;
-    const size_t off_v = (bq + 255) & ~size_t(255), off_t = off_v + ((bv + 255) & ~size_t(255));
-    const size_t off_w = off_t + ((bt + 255) & ~size_t(255));
+
+    // Column blocks of CH eigenvectors stream through NBUF device buffers: H2D on one copy
+    // stream, apply on `stream`, D2H on another, so PCIe traffic overlaps the kernel (columns
+    // are independent: each block's result is bitwise the unblocked one).
+    const int64_t CH = std::max<int64_t>(8, ((nev + 7) / 8 + 7) / 8 * 8);   // ~8 blocks
+    const int64_t nblk = (nev + CH - 1) / CH;
+    constexpr int NBUF = 3;
+    const size_t bqc = size_t(ldq) * CH * 8, bv = size_t(R) * nbw * 8, bt = size_t(R) * 8;
+    auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t off_v = 0, off_t = up(bv), off_w = off_t + up(bt), off_q = off_w + up(size_t(p.ws_bytes));
+    const size_t total = off_q + NBUF * up(bqc);
     // Keep the transient buffers cached in the device's default pool between calls: with the
     // default release threshold (0) every synchronising call would unmap and remap ~GBs.
     {
         int dev = 0;
         cudaMemPool_t pool;
         if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = 0, want = uint64_t(off_w + size_t(p.ws_bytes));
+            uint64_t thr = 0, want = uint64_t(total);
             if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess && thr < want)
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
         }
         cudaGetLastError();
     }
-    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), off_w + size_t(p.ws_bytes), s) != cudaSuccess)
-        return fail_cuda();
-    double *dQ = reinterpret_cast<double *>(buf), *dv = reinterpret_cast<double *>(buf + off_v);
-    double *dt = reinterpret_cast<double *>(buf + off_t);
+    char *buf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), total, s) != cudaSuccess) return fail_cuda();
+    double *dv = reinterpret_cast<double *>(buf + off_v), *dt = reinterpret_cast<double *>(buf + off_t);
     void *ws = p.ws_bytes ? buf + off_w : nullptr;
-    if (cudaMemcpyAsync(dv, hh_v, bv, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(dt, hh_tau, bt, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(dQ, Q, bq, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    double *dq[NBUF];
+    for (int i = 0; i < NBUF; i++) dq[i] = reinterpret_cast<double *>(buf + off_q + i * up(bqc));
+
+    cudaStream_t hs = nullptr, ds = nullptr;
+    std::vector<cudaEvent_t> ev_h2d(nblk), ev_comp(nblk), ev_d2h(nblk);
+    cudaEvent_t ev_ready = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming) == cudaSuccess;
+    for (int64_t c = 0; ok && c < nblk; c++)
+        ok = cudaEventCreateWithFlags(&ev_h2d[c], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev_comp[c], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev_d2h[c], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) rc = ELPA_B200_ERR_CUDA;
+    // the buffer is allocated on `s`: the copy streams start after it
+    if (rc == ELPA_B200_OK && (cudaEventRecord(ev_ready, s) != cudaSuccess ||
+                               cudaStreamWaitEvent(hs, ev_ready, 0) != cudaSuccess))
+        rc = ELPA_B200_ERR_CUDA;
+    if (rc == ELPA_B200_OK && (cudaMemcpyAsync(dv, hh_v, bv, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                               cudaMemcpyAsync(dt, hh_tau, bt, cudaMemcpyHostToDevice, s) != cudaSuccess))
         rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) rc = prepare_impl(p, n, dv, dt, ws, s);
-    if (rc == ELPA_B200_OK) rc = apply_impl(p, n, nbw, nev, dv, dt, ws, dQ, ldq, s);
-    if (rc == ELPA_B200_OK && cudaMemcpyAsync(Q, dQ, bq, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        rc = ELPA_B200_ERR_CUDA;
+    for (int64_t c = 0; rc == ELPA_B200_OK && c < nblk; c++) {
+        const int64_t c0 = c * CH, nc = std::min(CH, nev - c0);
+        double *d = dq[c % NBUF];
+        const size_t bytes = size_t(ldq) * nc * 8;
+        if ((c >= NBUF && cudaStreamWaitEvent(hs, ev_d2h[c - NBUF], 0) != cudaSuccess) ||
+            cudaMemcpyAsync(d, Q + c0 * ldq, bytes, cudaMemcpyHostToDevice, hs) != cudaSuccess ||
+            cudaEventRecord(ev_h2d[c], hs) != cudaSuccess || cudaStreamWaitEvent(s, ev_h2d[c], 0) != cudaSuccess) {
+            rc = ELPA_B200_ERR_CUDA;
+            break;
+        }
+        Plan pc;
+        if ((rc = make_plan(n, nbw, nc, opts, pc)) != ELPA_B200_OK) break;
+        if ((rc = apply_impl(pc, n, nbw, nc, dv, dt, ws, d, ldq, s)) != ELPA_B200_OK) break;
+        if (cudaEventRecord(ev_comp[c], s) != cudaSuccess || cudaStreamWaitEvent(ds, ev_comp[c], 0) != cudaSuccess ||
+            cudaMemcpyAsync(Q + c0 * ldq, d, bytes, cudaMemcpyDeviceToHost, ds) != cudaSuccess ||
+            cudaEventRecord(ev_d2h[c], ds) != cudaSuccess) {
+            rc = ELPA_B200_ERR_CUDA;
+            break;
+        }
+    }
+    // everything (including work already queued when an error stopped the loop) completes
+    // before the buffers go back to the pool
+    if (ds) cudaStreamSynchronize(ds);
+    if (hs) cudaStreamSynchronize(hs);
     if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
     if (cudaStreamSynchronize(s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    for (int64_t c = 0; c < nblk; c++) {
+        if (ev_h2d[c]) cudaEventDestroy(ev_h2d[c]);
+        if (ev_comp[c]) cudaEventDestroy(ev_comp[c]);
+        if (ev_d2h[c]) cudaEventDestroy(ev_d2h[c]);
+    }
+    if (ev_ready) cudaEventDestroy(ev_ready);
+    if (hs) cudaStreamDestroy(hs);
+    if (ds) cudaStreamDestroy(ds);
+    if (rc != ELPA_B200_OK) cudaGetLastError();
     return rc;
 }
 

@@ -163,14 +163,22 @@ def test_prepare_apply_two_phase(eb):
         assert _rel(dq.cpu().numpy(), want[half]) <= TOL
 
 
-def test_host_entry_point(eb):
+@pytest.mark.parametrize("n,nbw,nev", [(900, 64, 50), (1000, 32, 203), (777, 16, 7)])
+def test_host_entry_point(eb, n, nbw, nev):
+    """Host buffers, column blocks pipelined over copy streams: equal to the oracle, and
+    bitwise equal to the device-pointer call (column independence)."""
     import torch
-    n, nbw, nev = 900, 64, 50
     hv, tau, s, L, Q = synth_case(n, nbw, nev, 4)
     want = oracle.apply(hv, tau, s, L, Q)
     hq = torch.from_numpy(Q.copy()).pin_memory()
     eb.trans_ev_tridi_to_band_host(n, nbw, torch.from_numpy(hv).pin_memory(), torch.from_numpy(tau).pin_memory(), hq)
     assert _rel(hq.numpy(), want) <= TOL
+    dev = run_gpu(eb, n, nbw, hv, tau, Q)
+    assert np.array_equal(hq.numpy(), dev)
+    # pageable host memory works too (no overlap)
+    hq2 = torch.from_numpy(Q.copy())
+    eb.trans_ev_tridi_to_band_host(n, nbw, torch.from_numpy(hv), torch.from_numpy(tau), hq2)
+    assert np.array_equal(hq2.numpy(), dev)
 
 
 def test_full_size_C3_sampled_columns(eb):
