@@ -46,11 +46,11 @@ __host__ __device__ inline int64_t group_base(int64_t n, int64_t b8, int64_t m) 
 __host__ __device__ inline int64_t total_groups(int64_t n, int64_t b8, int64_t M) {
     return group_base(n, b8, M);
 }
-// doubles per prepared group.  DMMA layout (kind 0): dot B-fragments (lambda x 32 lanes x 2),
-// update B-fragments (same), -T fragments (32 x 2).  DFMA layout (kind 1): V row-major with a
-// padded row stride of 10 doubles (8*lambda rows), then -T^T row-major 8 x 8.
+// doubles per prepared group.  DMMA layout (kind 0): dot B-fragments of U = -V T (lambda x 32
+// lanes x 2), update B-fragments of V (same).  DFMA layout (kind 1): V row-major with a padded
+// row stride of 10 doubles (8*lambda rows), then -T^T row-major 8 x 8.
 __host__ __device__ inline int64_t blob_doubles(int64_t lambda, int kind = 0) {
-    return kind == 0 ? 128 * lambda + 64 : 80 * lambda + 64;
+    return kind == 0 ? 128 * lambda : 80 * lambda + 64;
 }
 
 }  // namespace elpa_b200

@@ -120,19 +120,18 @@ __device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
 // ---------------------------------------------------------------------------------------
 enum { KIND_DMMA = 0, KIND_DFMA = 1 };
 
-// FP64 tensor cores: 2*LAM + 2 + 2*LAM DMMA.8x8x4 per tile, no shuffles.  Blob layout
-// (prep kernel): dot B-fragments [LAM][32 lanes][2], update B-fragments [LAM][32][2] (== V
-// row-major 8 x 8 per chunk), -T fragments [32][2].
+// FP64 tensor cores: 2*LAM + 2*LAM DMMA.8x8x4 per tile, no shuffles.  Blob layout (prep
+// kernel): dot B-fragments of U = -V_g T [LAM][32 lanes][2], update B-fragments of V_g
+// [LAM][32][2] (== V_g row-major 8 x 8 per chunk).
 template <int LAM, int NCT>
 struct DmmaGroup {
-    static constexpr int BLOB = 128 * LAM + 64;
+    static constexpr int BLOB = 128 * LAM;
     __device__ __forceinline__ static void apply(double2 (&q)[NCT][LAM], const double *blob, uint32_t tilemask,
                                                  int lane) {
         const double2 *dotB = reinterpret_cast<const double2 *>(blob);
         const double2 *updB = dotB + 32 * LAM;
-        const double2 tf = dotB[64 * LAM + lane];
-        // Y^T = Q_W^T V_g: independent accumulators per tile (K half x, for NCT = 1, chunk
-        // parity) so every warp keeps >= 4 DMMA chains in flight
+        // W^T = Q_W^T U (= -(T^T V_g^T Q_W)^T): independent accumulators per tile (K half x,
+        // for NCT = 1, chunk parity) so every warp keeps >= 4 DMMA chains in flight
         constexpr int NACC = (NCT >= 2) ? 2 : 4;
         double2 y[NCT][NACC];
 #pragma unroll
@@ -151,19 +150,16 @@ struct DmmaGroup {
                 dmma(yb.x, yb.y, q[t][i].y, vb.y);
             }
         }
-        // W^T = Y^T (-T)
         double2 w[NCT];
 #pragma unroll
         for (int t = 0; t < NCT; t++) {
             if (!((tilemask >> t) & 1)) continue;
-            double ya = y[t][0].x + y[t][1].x, yb = y[t][0].y + y[t][1].y;
+            w[t].x = y[t][0].x + y[t][1].x;
+            w[t].y = y[t][0].y + y[t][1].y;
             if (NACC == 4) {
-                ya += y[t][NACC - 2].x + y[t][NACC - 1].x;
-                yb += y[t][NACC - 2].y + y[t][NACC - 1].y;
+                w[t].x += y[t][NACC - 2].x + y[t][NACC - 1].x;
+                w[t].y += y[t][NACC - 2].y + y[t][NACC - 1].y;
             }
-            w[t] = make_double2(0.0, 0.0);
-            dmma(w[t].x, w[t].y, ya, tf.x);
-            dmma(w[t].x, w[t].y, yb, tf.y);
         }
         // Q_W^T += W^T V_g^T
 #pragma unroll

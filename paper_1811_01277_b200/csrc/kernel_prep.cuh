@@ -5,10 +5,9 @@
 // starting at window row 7-a, v_0 = 1, zero outside [7-a, 7-a+L)) and the forward compact-WY
 // factor T (dlarft, upper triangular: H_0 H_1 ... H_7 = I - V T V^T), and store them as
 // ready-to-use m8n8k4 FP64 MMA B-fragments, lane-ordered so each warp reads a group with
-// conflict-free 16-byte shared-memory loads:
-//   dotB[i][lane] = (V[8i + 2(lane%4)][lane/4],  V[8i + 2(lane%4) + 1][lane/4])
+// conflict-free 16-byte shared-memory loads, with U = -V T folded in:
+//   dotB[i][lane] = (U[8i + 2(lane%4)][lane/4],  U[8i + 2(lane%4) + 1][lane/4])
 //   updB[i][lane] = (V[8i + lane/4][2(lane%4)],  V[8i + lane/4][2(lane%4) + 1])
-//   tf[lane]      = (-T[2(lane%4)][lane/4],      -T[2(lane%4) + 1][lane/4])
 // One warp per group.  Missing reflectors (j < 0 or j > J_m) get tau = 0 (identity).
 // KIND 1 (DFMA kernel) instead writes V row-major with row stride 10 and M = -T^T row-major.
 #pragma once
@@ -79,20 +78,23 @@ prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__res
         for (int e = lane; e < 64; e += 32) blob[WR * 10 + e] = -Ts[warp][e & 7][e >> 3];
         return;
     }
+    // U = -V T (window rows x 8): the dot phase then yields W^T = Q_W^T U directly
+    // (W = -T^T V^T Q_W), so the apply kernel needs no separate T step
+    auto U = [&](int w, int a) {
+        double acc = 0.0;
+        for (int p = 0; p <= a; p++) acc = fma(V[w][p], Ts[warp][p][a], acc);
+        return -acc;
+    };
     const int kq = lane & 3, gq = lane >> 2;
     for (int i = 0; i < LAM; i++) {
         double2 d, u;
-        d.x = V[8 * i + 2 * kq][gq];
-        d.y = V[8 * i + 2 * kq + 1][gq];
+        d.x = U(8 * i + 2 * kq, gq);
+        d.y = U(8 * i + 2 * kq + 1, gq);
         u.x = V[8 * i + gq][2 * kq];
         u.y = V[8 * i + gq][2 * kq + 1];
         reinterpret_cast<double2 *>(blob)[i * 32 + lane] = d;
         reinterpret_cast<double2 *>(blob + 64 * LAM)[i * 32 + lane] = u;
     }
-    double2 tf;
-    tf.x = -Ts[warp][2 * kq][gq];
-    tf.y = -Ts[warp][2 * kq + 1][gq];
-    reinterpret_cast<double2 *>(blob + 128 * LAM)[lane] = tf;
 }
 
 }  // namespace elpa_b200

@@ -96,11 +96,11 @@ def test_describe_and_workspace():
     k, desc = eb.describe(100, 6, 10)
     assert k == 1 and "kernel=reference" in desc
     assert eb.describe(2, 4, 2)[0] == 0
-    # workspace = groups * (128*lambda + 64) doubles
+    # workspace = groups * 128*lambda doubles (DMMA fragments of U = -V T and V)
     n, b = 4096, 32
     b8, lam = b // 8, b // 8 + 1
     M = (n - 3) // b + 1
     G0 = ((n - 2) >> 3) + 1
     groups = sum(G0 - m * b8 for m in range(M))
-    assert eb.workspace_bytes(n, b) == groups * (128 * lam + 64) * 8
+    assert eb.workspace_bytes(n, b) == groups * 128 * lam * 8
     assert eb.workspace_bytes(100, 6) == 0

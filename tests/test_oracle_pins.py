@@ -320,3 +320,7 @@ def test_P12_compact_group_equals_sequential(k):
         T[:a, a] = -tau[a] * T[:a, :a] @ G[:a, a]
     comp = Q - V @ (T.T @ (V.T @ Q))
     assert np.abs(comp - seq).max() < 1e-13
+    # the form the DMMA kernel evaluates: U = -V T prepared once, W^T = Q^T U, Q += V W
+    U = -V @ T
+    comp_u = Q + V @ (U.T @ Q)
+    assert np.abs(comp_u - seq).max() < 1e-13
