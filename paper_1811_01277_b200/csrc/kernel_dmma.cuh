@@ -126,13 +126,17 @@ enum { KIND_DMMA = 0, KIND_DFMA = 1 };
 template <int LAM, int NCT>
 struct DmmaGroup {
     static constexpr int BLOB = 128 * LAM;
-    __device__ __forceinline__ static void apply(double2 (&q)[NCT][LAM], const double *blob, uint32_t tilemask,
+    // tilemask is ignored: a tile past the end of Q holds zeros (masked loads) and is never
+    // stored, so computing it costs nothing but keeps every DMMA unpredicated (a predicated
+    // mma.sync needs WARPSYNC + NOP padding around it)
+    __device__ __forceinline__ static void apply(double2 (&q)[NCT][LAM], const double *blob, uint32_t,
                                                  int lane) {
         const double2 *dotB = reinterpret_cast<const double2 *>(blob);
         const double2 *updB = dotB + 32 * LAM;
-        // W^T = Q_W^T U (= -(T^T V_g^T Q_W)^T): independent accumulators per tile (K half x,
-        // for NCT = 1, chunk parity) so every warp keeps >= 4 DMMA chains in flight
-        constexpr int NACC = (NCT >= 2) ? 2 : 4;
+        // W^T = Q_W^T U (= -(T^T V_g^T Q_W)^T).  With NCT >= 2 one accumulator chain per tile
+        // (the tiles interleave, so consecutive dependent DMMAs are >= NCT issues apart and no
+        // DADD combine sits between the phases); NCT = 1 splits the K halves into 2 chains.
+        constexpr int NACC = (NCT >= 2) ? 1 : 2;
         double2 y[NCT][NACC];
 #pragma unroll
         for (int t = 0; t < NCT; t++)
@@ -143,9 +147,8 @@ struct DmmaGroup {
             const double2 vb = dotB[i * 32 + lane];
 #pragma unroll
             for (int t = 0; t < NCT; t++) {
-                if (!((tilemask >> t) & 1)) continue;
-                double2 &ya = y[t][(NACC == 4) ? 2 * (i & 1) : 0];
-                double2 &yb = y[t][(NACC == 4) ? 2 * (i & 1) + 1 : 1];
+                double2 &ya = y[t][0];
+                double2 &yb = y[t][NACC - 1];
                 dmma(ya.x, ya.y, q[t][i].x, vb.x);
                 dmma(yb.x, yb.y, q[t][i].y, vb.y);
             }
@@ -153,12 +156,10 @@ struct DmmaGroup {
         double2 w[NCT];
 #pragma unroll
         for (int t = 0; t < NCT; t++) {
-            if (!((tilemask >> t) & 1)) continue;
-            w[t].x = y[t][0].x + y[t][1].x;
-            w[t].y = y[t][0].y + y[t][1].y;
-            if (NACC == 4) {
-                w[t].x += y[t][NACC - 2].x + y[t][NACC - 1].x;
-                w[t].y += y[t][NACC - 2].y + y[t][NACC - 1].y;
+            w[t] = y[t][0];
+            if (NACC == 2) {
+                w[t].x += y[t][1].x;
+                w[t].y += y[t][1].y;
             }
         }
         // Q_W^T += W^T V_g^T
@@ -167,7 +168,6 @@ struct DmmaGroup {
             const double2 ub = updB[i * 32 + lane];
 #pragma unroll
             for (int t = 0; t < NCT; t++) {
-                if (!((tilemask >> t) & 1)) continue;
                 dmma(q[t][i].x, q[t][i].y, w[t].x, ub.x);
                 dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
             }
