@@ -99,9 +99,12 @@ size_t dmma_smem(int b8, int D, int CW, int NCT, int K, int kind) {
 void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int &K) {
     (void)ntile; (void)M;
     K = 1;
-    // best of 5 per shape (profiles/shape_sweep_r01_final.jsonl)
-    if (b8 >= 8) { D = 1; CW = 2; NCT = 2; }   // nbw = 64: C3 26.3, C4 24.4, C3/8 shard 24.7 TF/s
-    else { D = 2; CW = 4; NCT = 2; }           // nbw <= 32: C2 18.9 TF/s
+    // best of 5 per shape (profiles/shape_sweep_r01_final2.jsonl), TF/s:
+    //                 C2    C4    C3/8  C3/4  C3    C5/8
+    //   (1,2,4,1)   17.8  24.8  25.8  27.1  28.1  27.7
+    //   (2,2,2,1)   19.4  25.7  26.6  27.4  27.7  27.5
+    if (b8 >= 8 && ntile >= 2000) { D = 1; CW = 2; NCT = 4; }
+    else { D = 2; CW = 2; NCT = 2; }
 }
 
 int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
