@@ -14,12 +14,11 @@
 //     one 8-row chunk: warp 0 takes the next chunk from HBM, warp d>0 takes the chunk warp
 //     d-1 emitted (shared-memory hand-off), warp D-1's emitted chunk goes back to HBM.
 //     Each Q row therefore crosses HBM once per D depths.
-//   * Per group and tile (all on DMMA):
-//        Y^T  = Q_W^T V_g              2*lambda MMAs (K = rows)          [dot products, a4]
-//        W^T  = Y^T (-T)               2 MMAs        (K = reflectors)    [recurrence,   a5]
-//        Q_W^T += W^T V_g^T            2*lambda MMAs (K = reflectors)    [rank-8 update, a6]
-//     The accumulator layout of each product is directly the A-operand layout of the next
-//     (K index permuted to match), so no shuffles are needed anywhere.
+//   * Per group and tile (all on DMMA), with U = -V_g T prepared by the prep kernel:
+//        W^T  = Q_W^T U                2*lambda MMAs (K = rows)   [dot products + recurrence, a4/a5]
+//        Q_W^T += W^T V_g^T            2*lambda MMAs (K = reflectors)           [rank-8 update, a6]
+//     The dot accumulator layout is directly the update's A-operand layout (K index permuted
+//     to match), so no shuffles are needed anywhere.
 //   * Prepared fragments of the D groups of the next step are fetched with cp.async.bulk
 //     into a 2-stage shared-memory ring completed on an mbarrier (one elected thread).
 #pragma once
