@@ -307,7 +307,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
     constexpr int B = 8 * B8;
     constexpr int LAG = K + 1;                             // groups depth m+1 trails depth m
     constexpr int SPAN = LAM + K;                          // chunk distance between stacked windows
-    constexpr int PUB = (K >= 4) ? 4 : 16 / K;             // publish progress every PUB steps
+    constexpr int PUB = 32;                                // publish progress every PUB steps
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sblob = reinterpret_cast<double *>(smem_raw);                                        // [S][K][D][BLOB]
@@ -451,7 +451,8 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                     for (int t = 0; t < NCT; t++)
                         store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
                     // publish: every chunk >= cbot is final for the next pass
-                    if (j == K - 1 && (st % PUB) == PUB - 1 && cbot <= C0 + 1 && cbot >= 0) {
+                    // (also right when chunk C0 becomes final, so a waiting next pass starts at once)
+                    if (j == K - 1 && ((st % PUB) == PUB - 1 || cbot == C0) && cbot <= C0 + 1 && cbot >= 0) {
                         __threadfence();
                         __syncwarp();
                         if (lane == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
