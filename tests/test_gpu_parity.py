@@ -238,3 +238,40 @@ def test_dfma_real_C1_residual(eb):
     got = run_gpu(eb, 512, 16, case["hh_v"], case["hh_tau"], case["Qin"], opts=dict(kernel=eb.KERNEL_DFMA))
     assert _rel(got, case["Qref"]) <= TOL
     assert oracle.residual(case["band"], got, case["lam"]) <= 1e-13
+
+
+@pytest.mark.parametrize("kernel,shape", [(2, None), (2, (2, 2, 2, 1)), (2, (4, 2, 4, 1)), (2, (1, 2, 4, 1)),
+                                          (3, None), (1, None)])
+@pytest.mark.parametrize("n,nbw,nev", [(301, 64, 45), (200, 16, 33), (97, 8, 9)])
+def test_guard_bands(eb, kernel, shape, n, nbw, nev):
+    """compute-sanitizer is closed on this pool, so out-of-bounds accesses are caught with
+    guard bands: Q sits inside a larger allocation whose margins (and the ldq padding rows)
+    hold a NaN sentinel.  Any stray write changes a guard word; any stray read of a guard
+    propagates NaN into the result."""
+    import torch
+    ldq = n + (n & 1) + 2
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 17 + n, ldq=ldq)
+    Q[:, n:] = np.nan
+    want = oracle.apply(hv, tau, s, L, Q[:, :n].copy())
+    G = 4096
+    big = torch.full((G + nev * ldq + G,), float("nan"), dtype=torch.float64, device="cuda")
+    big[G:G + nev * ldq] = torch.from_numpy(Q.reshape(-1)).cuda()
+    dq = big[G:G + nev * ldq].view(nev, ldq)
+    opts = None if shape is None else dict(kernel=kernel, depth_warps=shape[0], col_warps=shape[1],
+                                           tiles_per_warp=shape[2], groups_per_step=shape[3])
+    if shape is None and kernel != 2:
+        opts = dict(kernel=kernel)
+    hvd = torch.full((hv.shape[0] + 2, nbw), float("nan"), dtype=torch.float64, device="cuda")
+    hvd[1:-1] = torch.from_numpy(hv).cuda()
+    for r, Lr in enumerate(L):
+        hvd[1 + r, Lr:] = float("nan")              # elements >= L are never read
+    taud = torch.full((len(tau) + 2,), float("nan"), dtype=torch.float64, device="cuda")
+    taud[1:-1] = torch.from_numpy(tau).cuda()
+    eb.trans_ev_tridi_to_band(n, nbw, hvd[1:-1], taud[1:-1], dq, opts=opts)
+    torch.cuda.synchronize()
+    out = big.cpu().numpy()
+    assert np.all(np.isnan(out[:G])) and np.all(np.isnan(out[G + nev * ldq:]))
+    got = out[G:G + nev * ldq].reshape(nev, ldq)
+    assert np.all(np.isnan(got[:, n:]))
+    assert np.isfinite(got[:, :n]).all()
+    assert _rel(got[:, :n], want) <= TOL
