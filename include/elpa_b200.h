@@ -70,7 +70,8 @@ enum {
     ELPA_B200_KERNEL_REFERENCE = 1, /* one thread per column, exact reverse generation order,
                                        no FMA contraction: bitwise equal to the CPU oracle */
     ELPA_B200_KERNEL_DMMA = 2,      /* k = 8 compact-WY groups on FP64 tensor cores (DMMA),
-                                       depth-pipelined row windows; requires nbw % 8 == 0 */
+                                       depth-pipelined row windows; nbw % 8 == 0, nbw <= 128
+                                       (AUTO picks it then, else REFERENCE) */
     ELPA_B200_KERNEL_DFMA = 3       /* the same groups and schedule on FP64 CUDA cores (DFMA +
                                        warp shuffles): the measured alternative to DMMA */
 };

@@ -53,11 +53,10 @@ int smem_optin() {
     return v > 0 ? v : 232448;
 }
 
-bool b8_supported(int64_t nbw) {
-    if (nbw % 8) return false;
-    const int64_t b8 = nbw / 8;
-    return b8 == 1 || b8 == 2 || b8 == 4 || b8 == 8;
-}
+// nbw = 8*b8 with b8 in 1..16 runs on the DMMA path; {1,2,4,8} (nbw 8/16/32/64) get the full
+// shape menu, the other multiples of 8 up to 128 a small one (compile-time budget)
+bool b8_full_menu(int b8) { return b8 == 1 || b8 == 2 || b8 == 4 || b8 == 8; }
+bool b8_supported(int64_t nbw) { return nbw % 8 == 0 && nbw >= 8 && nbw <= 128; }
 
 // (D, CW, NCT) menu of compiled DMMA configurations
 // (D depth warps, CW column warps, NCT tiles per warp, K groups per step)
@@ -73,6 +72,19 @@ constexpr Shape kShapes[] = {ELPA_SHAPES(ELPA_SHAPE_ENTRY)};
 // the DFMA comparison kernel is compiled for a smaller menu
 #define ELPA_DFMA_SHAPES(X) X(1, 2, 2, 1) X(2, 2, 2, 1) X(1, 4, 2, 1) X(2, 4, 2, 1) X(1, 2, 4, 1) X(2, 2, 4, 1)
 constexpr Shape kDfmaShapes[] = {ELPA_DFMA_SHAPES(ELPA_SHAPE_ENTRY)};
+
+#define ELPA_SMALL_SHAPES(X) X(2, 2, 2, 1) X(1, 2, 2, 1)
+constexpr Shape kSmallShapes[] = {ELPA_SMALL_SHAPES(ELPA_SHAPE_ENTRY)};
+
+bool shape_compiled(bool dfma, int D, int CW, int NCT, int K);
+bool shape_compiled(bool dfma, int D, int CW, int NCT, int K, int b8) {
+    if (!b8_full_menu(b8)) {
+        for (const Shape &s : kSmallShapes)
+            if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
+        return false;
+    }
+    return shape_compiled(dfma, D, CW, NCT, K);
+}
 
 bool shape_compiled(bool dfma, int D, int CW, int NCT, int K) {
     if (dfma) {
@@ -103,8 +115,8 @@ void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int
     //                 C2    C4    C3/8  C3/4  C3    C5/8
     //   (1,2,4,1)   17.8  24.8  25.8  27.1  28.1  27.7
     //   (2,2,2,1)   19.4  25.7  26.6  27.4  27.7  27.5
-    if (b8 >= 8 && ntile >= 2000) { D = 1; CW = 2; NCT = 4; }
-    else { D = 2; CW = 2; NCT = 2; }
+    if (b8 == 8 && ntile >= 2000) { D = 1; CW = 2; NCT = 4; }
+    else { D = 2; CW = 2; NCT = 2; }   // also the default of the small menu (nbw != 8/16/32/64)
 }
 
 int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan &p) {
@@ -133,7 +145,7 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
         if (K == 0) K = Ka;
     }
     if (K == 0) K = 1;
-    if (!shape_compiled(kernel == ELPA_B200_KERNEL_DFMA, D, CW, NCT, K)) return ELPA_B200_ERR_ARG;
+    if (!shape_compiled(kernel == ELPA_B200_KERNEL_DFMA, D, CW, NCT, K, p.b8)) return ELPA_B200_ERR_ARG;
     p.D = D; p.CW = CW; p.NCT = NCT; p.K = K;
     p.grid_req = o ? o->grid_ctas : 0;
     if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
@@ -226,10 +238,18 @@ int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, doub
 #define ELPA_DFMA_SHAPE(D_, CW_, NCT_, K_)                     \
     if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
         return launch_dmma_shape<KIND_DFMA, B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
-    if (p.kernel == ELPA_B200_KERNEL_DFMA) {
-        ELPA_DFMA_SHAPES(ELPA_DFMA_SHAPE)
+    if constexpr (B8 == 1 || B8 == 2 || B8 == 4 || B8 == 8) {
+        if (p.kernel == ELPA_B200_KERNEL_DFMA) {
+            ELPA_DFMA_SHAPES(ELPA_DFMA_SHAPE)
+        } else {
+            ELPA_SHAPES(ELPA_SHAPE)
+        }
     } else {
-        ELPA_SHAPES(ELPA_SHAPE)
+        if (p.kernel == ELPA_B200_KERNEL_DFMA) {
+            ELPA_SMALL_SHAPES(ELPA_DFMA_SHAPE)
+        } else {
+            ELPA_SMALL_SHAPES(ELPA_SHAPE)
+        }
     }
 #undef ELPA_SHAPE
 #undef ELPA_DFMA_SHAPE
@@ -241,10 +261,12 @@ int prepare_impl(const Plan &p, int64_t n, const double *hh_v, const double *hh_
     double *w = static_cast<double *>(ws);
     const int kind = p.kernel == ELPA_B200_KERNEL_DFMA ? 1 : 0;
     switch (p.b8) {
-        case 1: return launch_prep<1>(n, hh_v, hh_tau, w, kind, s);
-        case 2: return launch_prep<2>(n, hh_v, hh_tau, w, kind, s);
-        case 4: return launch_prep<4>(n, hh_v, hh_tau, w, kind, s);
-        case 8: return launch_prep<8>(n, hh_v, hh_tau, w, kind, s);
+#define ELPA_PREP_CASE(B8_) \
+    case B8_: return launch_prep<B8_>(n, hh_v, hh_tau, w, kind, s);
+        ELPA_PREP_CASE(1) ELPA_PREP_CASE(2) ELPA_PREP_CASE(3) ELPA_PREP_CASE(4) ELPA_PREP_CASE(5) ELPA_PREP_CASE(6)
+        ELPA_PREP_CASE(7) ELPA_PREP_CASE(8) ELPA_PREP_CASE(9) ELPA_PREP_CASE(10) ELPA_PREP_CASE(11)
+        ELPA_PREP_CASE(12) ELPA_PREP_CASE(13) ELPA_PREP_CASE(14) ELPA_PREP_CASE(15) ELPA_PREP_CASE(16)
+#undef ELPA_PREP_CASE
     }
     return ELPA_B200_ERR_ARG;
 }
@@ -257,10 +279,13 @@ int apply_impl(const Plan &p, int64_t n, int64_t nbw, int64_t nev, const double 
     }
     const double *w = static_cast<const double *>(ws);
     switch (p.b8) {
-        case 1: return launch_dmma_b8<1>(p, n, nev, w, Q, ldq, s);
-        case 2: return launch_dmma_b8<2>(p, n, nev, w, Q, ldq, s);
-        case 4: return launch_dmma_b8<4>(p, n, nev, w, Q, ldq, s);
-        case 8: return launch_dmma_b8<8>(p, n, nev, w, Q, ldq, s);
+#define ELPA_APPLY_CASE(B8_) \
+    case B8_: return launch_dmma_b8<B8_>(p, n, nev, w, Q, ldq, s);
+        ELPA_APPLY_CASE(1) ELPA_APPLY_CASE(2) ELPA_APPLY_CASE(3) ELPA_APPLY_CASE(4) ELPA_APPLY_CASE(5)
+        ELPA_APPLY_CASE(6) ELPA_APPLY_CASE(7) ELPA_APPLY_CASE(8) ELPA_APPLY_CASE(9) ELPA_APPLY_CASE(10)
+        ELPA_APPLY_CASE(11) ELPA_APPLY_CASE(12) ELPA_APPLY_CASE(13) ELPA_APPLY_CASE(14) ELPA_APPLY_CASE(15)
+        ELPA_APPLY_CASE(16)
+#undef ELPA_APPLY_CASE
     }
     return ELPA_B200_ERR_ARG;
 }

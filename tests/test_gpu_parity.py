@@ -275,3 +275,21 @@ def test_guard_bands(eb, kernel, shape, n, nbw, nev):
     assert np.all(np.isnan(got[:, n:]))
     assert np.isfinite(got[:, :n]).all()
     assert _rel(got[:, :n], want) <= TOL
+
+
+@pytest.mark.parametrize("nbw", [24, 40, 48, 56, 72, 96, 128, 20, 130])
+def test_nbw_range(eb, nbw):
+    """nbw = any multiple of 8 up to 128 runs the DMMA path (small shape menu off 8/16/32/64);
+    other nbw run the bit-exact GPU reference kernel."""
+    n, nev = 523, 37
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 5 + nbw)
+    want = oracle.apply(hv, tau, s, L, Q)
+    k, desc = eb.describe(n, nbw, nev)
+    assert ("kernel=dmma" in desc) == (nbw % 8 == 0 and nbw <= 128)
+    got = run_gpu(eb, n, nbw, hv, tau, Q)
+    if "kernel=dmma" in desc:
+        assert _rel(got, want) <= TOL
+        got1 = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=2, depth_warps=1, col_warps=2, tiles_per_warp=2))
+        assert _rel(got1, want) <= TOL
+    else:
+        assert np.array_equal(got, want)
