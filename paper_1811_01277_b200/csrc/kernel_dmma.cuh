@@ -364,6 +364,13 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         const int NT = G + dmax * LAG;                     // group-times of this item
         const int nsteps = (NT + K - 1) / K;
 
+        // publish steps: every PUB steps, and the step whose emission finalises chunk C0 (so a
+        // next pass waiting for its first window starts at once); only while the deepest warps'
+        // emissions are real chunks
+        auto pub_step = [&](int st) {
+            const int cbot = C0 - (st * K + K - 1) + (D - 1) * SPAN + LAM - 1;
+            return ((st % PUB) == PUB - 1 || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
+        };
         auto group_valid = [&](int tau, int dd) {
             const int g = G - 1 - tau + dd * LAG;
             return dd <= dmax && tau < NT && g >= 0 && g < G - dd * B8;
@@ -450,13 +457,9 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
 #pragma unroll
                     for (int t = 0; t < NCT; t++)
                         store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
-                    // publish: every chunk >= cbot is final for the next pass
-                    // (also right when chunk C0 becomes final, so a waiting next pass starts at once)
-                    if (j == K - 1 && ((st % PUB) == PUB - 1 || cbot == C0) && cbot <= C0 + 1 && cbot >= 0) {
-                        __threadfence();
-                        __syncwarp();
-                        if (lane == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
-                    }
+                    // on publish steps the emitted stores are fenced here; thread 0 publishes after
+                    // the step barrier, when EVERY column warp of the item has stored its chunks
+                    if (pub_step(st)) __threadfence();
                 } else {
 #pragma unroll
                     for (int t = 0; t < NCT; t++) shand[hslot(st & 1, d + 1, j, t)] = q[t][LAM - 1];
@@ -477,6 +480,11 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             }
             if (done) break;
             __syncthreads();
+            if (threadIdx.x == 0 && pub_step(st)) {
+                // every chunk >= the deepest warps' last emission is final for the next pass
+                const int cbot = C0 - (st * K + K - 1) + (D - 1) * SPAN + LAM - 1;
+                st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
+            }
         }
         if (d == 0) cp_async_wait<0>();   // drain any unused intake before slot reuse
         __syncthreads();                  // the last step's hand-off writes are visible below

@@ -293,3 +293,19 @@ def test_nbw_range(eb, nbw):
         assert _rel(got1, want) <= TOL
     else:
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 4, 1), (2, 2, 2, 1), (1, 4, 2, 1), (2, 2, 4, 1)])
+@pytest.mark.parametrize("grid", [2, 3, 5, 0])
+def test_progress_publish_multi_column_warps(eb, shape, grid):
+    """Items of consecutive depth passes of one tile group run concurrently on different CTAs
+    while each item has several column warps: the next pass may only read a chunk once EVERY
+    column warp of the producing item has stored it (regression: per-warp publishing raced)."""
+    D, CW, NCT, K = shape
+    n, nbw, nev = 700, 64, CW * NCT * 8          # one tile group: all items chain on one x
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 41 + grid)
+    want = oracle.apply(hv, tau, s, L, Q)
+    for kernel in (2, 3) if shape in [(1, 2, 4, 1), (2, 2, 2, 1), (1, 4, 2, 1), (2, 2, 4, 1)] else (2,):
+        got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=kernel, depth_warps=D, col_warps=CW,
+                                                         tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
+        assert _rel(got, want) <= TOL, kernel
