@@ -272,10 +272,13 @@ struct DmmaCfg {
     static constexpr size_t SMEM_HAND = size_t(2) * D * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
-    // DFMA policy: cap registers near 168 (unbounded, ptxas hoists every shared V load of a
-    // group and spills ~1 KB); the DMMA policy needs no bound
-    static constexpr int MINB_DFMA = 65536 / (THREADS * 168);
-    static constexpr int MINB = (KIND == KIND_DFMA && MINB_DFMA > 1) ? MINB_DFMA : 1;
+    // Occupancy intent as a launch bound.  DMMA: the register window (4*LAM*NCT) + ~80, so an
+    // incidental code change cannot let ptxas spread into a CTA/SM fewer (seen: 138 -> 183
+    // registers, 3 -> 2 CTAs/SM, 28.1 -> 21.0 TF/s).  DFMA: cap near 168 (unbounded, ptxas
+    // hoists every shared V load of a group and spills ~1 KB).
+    static constexpr int REG_EST = (KIND == KIND_DFMA) ? 168 : 4 * LAM * NCT + 80;
+    static constexpr int MINB_RAW = 65536 / (THREADS * REG_EST);
+    static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
 };
 
 // Progress word of work item (x, p): e means pass p of tile group x has
