@@ -310,7 +310,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
     constexpr int B = 8 * B8;
     constexpr int LAG = K + 1;                             // groups depth m+1 trails depth m
     constexpr int SPAN = LAM + K;                          // chunk distance between stacked windows
-    constexpr int PUB = 32;                                // publish progress every PUB steps
+    constexpr int PUB = 128;                               // steady-state publish period (steps)
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sblob = reinterpret_cast<double *>(smem_raw);                                        // [S][K][D][BLOB]
@@ -367,12 +367,13 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         const int NT = G + dmax * LAG;                     // group-times of this item
         const int nsteps = (NT + K - 1) / K;
 
-        // publish steps: every PUB steps, and the step whose emission finalises chunk C0 (so a
-        // next pass waiting for its first window starts at once); only while the deepest warps'
-        // emissions are real chunks
+        // publish steps: every 8 steps early in the item (a next pass may be right behind), every
+        // PUB steps later (it then lags by hundreds of steps), and the step whose emission
+        // finalises chunk C0; only while the deepest warps' emissions are real chunks
         auto pub_step = [&](int st) {
             const int cbot = C0 - (st * K + K - 1) + (D - 1) * SPAN + LAM - 1;
-            return ((st % PUB) == PUB - 1 || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
+            const bool every = (st < 128) ? ((st & 7) == 7) : ((st % PUB) == PUB - 1);
+            return (every || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
         };
         auto group_valid = [&](int tau, int dd) {
             const int g = G - 1 - tau + dd * LAG;
@@ -460,9 +461,9 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
 #pragma unroll
                     for (int t = 0; t < NCT; t++)
                         store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
-                    // on publish steps the emitted stores are fenced here; thread 0 publishes after
-                    // the step barrier, when EVERY column warp of the item has stored its chunks
-                    if (pub_step(st)) __threadfence();
+                    // thread 0 publishes after the step barrier, when EVERY column warp of the item
+                    // has stored its chunks (stores -> bar.sync -> st.release.gpu -> consumer's
+                    // ld.acquire.gpu: causality is transitive through the CTA barrier)
                 } else {
 #pragma unroll
                     for (int t = 0; t < NCT; t++) shand[hslot(st & 1, d + 1, j, t)] = q[t][LAM - 1];
