@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -44,6 +45,18 @@ int sm_count() {
 int fail_cuda() {
     cudaGetLastError();
     return ELPA_B200_ERR_CUDA;
+}
+
+// Progress-publish period in steps: each publish is a release fence on the
+// CTA's critical path, but a next pass chained right behind waits for it.  Development
+// override: ELPA_B200_PUB.
+int pub_period() {
+    static int v = [] {
+        const char *e = getenv("ELPA_B200_PUB");
+        int x = e ? atoi(e) : 16;
+        return x >= 1 ? x : 16;
+    }();
+    return v;
 }
 
 int smem_optin() {
@@ -222,7 +235,8 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
         apply_dmma_kernel<KIND, B8, D, CW, NCT, K><<<unsigned(grid), DmmaCfg<KIND, B8, D, CW, NCT, K>::THREADS,
-                                                     DmmaCfg<KIND, B8, D, CW, NCT, K>::SMEM, s>>>(n, nev, ws, Q, ldq, prog);
+                                                     DmmaCfg<KIND, B8, D, CW, NCT, K>::SMEM, s>>>(n, nev, ws, Q, ldq, prog,
+                                                                                                  pub_period());
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     }
     if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;

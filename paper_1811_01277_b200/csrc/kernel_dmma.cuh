@@ -301,7 +301,7 @@ constexpr uint64_t kPassDone = ~0ull;
 template <int KIND, int B8, int D, int CW, int NCT, int K>
 __global__ void __launch_bounds__(DmmaCfg<KIND, B8, D, CW, NCT, K>::THREADS, DmmaCfg<KIND, B8, D, CW, NCT, K>::MINB)
 apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, double *Q, int64_t ldq,
-                  uint64_t *prog) {
+                  uint64_t *prog, int pub_period) {
     using Cfg = DmmaCfg<KIND, B8, D, CW, NCT, K>;
     constexpr int LAM = Cfg::LAM;
     constexpr int BLOB = Cfg::BLOB;
@@ -310,7 +310,6 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
     constexpr int B = 8 * B8;
     constexpr int LAG = K + 1;                             // groups depth m+1 trails depth m
     constexpr int SPAN = LAM + K;                          // chunk distance between stacked windows
-    constexpr int PUB = 128;                               // steady-state publish period (steps)
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sblob = reinterpret_cast<double *>(smem_raw);                                        // [S][K][D][BLOB]
@@ -367,12 +366,12 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         const int NT = G + dmax * LAG;                     // group-times of this item
         const int nsteps = (NT + K - 1) / K;
 
-        // publish steps: every 8 steps early in the item (a next pass may be right behind), every
-        // PUB steps later (it then lags by hundreds of steps), and the step whose emission
-        // finalises chunk C0; only while the deepest warps' emissions are real chunks
+        // publish steps: every pub_period steps (host-chosen) and the step whose emission
+        // finalises chunk C0 (a next pass waiting for its first window starts at once); only
+        // while the deepest warps' emissions are real chunks
         auto pub_step = [&](int st) {
             const int cbot = C0 - (st * K + K - 1) + (D - 1) * SPAN + LAM - 1;
-            const bool every = (st < 128) ? ((st & 7) == 7) : ((st % PUB) == PUB - 1);
+            const bool every = (st % pub_period) == pub_period - 1;
             return (every || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
         };
         auto group_valid = [&](int tau, int dd) {
