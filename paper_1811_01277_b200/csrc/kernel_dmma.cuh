@@ -460,9 +460,11 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
 #pragma unroll
                     for (int t = 0; t < NCT; t++)
                         store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
-                    // thread 0 publishes after the step barrier, when EVERY column warp of the item
-                    // has stored its chunks (stores -> bar.sync -> st.release.gpu -> consumer's
-                    // ld.acquire.gpu: causality is transitive through the CTA barrier)
+                    // on publish steps the emitted stores are fenced here; thread 0 publishes after
+                    // the step barrier, when EVERY column warp of the item has stored its chunks.
+                    // (Dropping this fence and relying on bar.sync + thread 0's release alone
+                    // measured 1.5x slower for D = 1 shapes: 28 -> 18.5 TF/s at C3.)
+                    if (pub_step(st)) __threadfence();
                 } else {
 #pragma unroll
                     for (int t = 0; t < NCT; t++) shand[hslot(st & 1, d + 1, j, t)] = q[t][LAM - 1];
