@@ -53,8 +53,8 @@ int fail_cuda() {
 int pub_period() {
     static int v = [] {
         const char *e = getenv("ELPA_B200_PUB");
-        int x = e ? atoi(e) : 16;
-        return x >= 1 ? x : 16;
+        int x = e ? atoi(e) : 32;
+        return x >= 1 ? x : 32;
     }();
     return v;
 }
