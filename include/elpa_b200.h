@@ -139,6 +139,41 @@ int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev,
 int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *opts,
                        char *buf, size_t buflen);
 
+/* ---------------------------------------------------------------------------------------
+ * Autotuning of the back-transformation's blocking parameters.
+ * Mirrors ELPA's autotuning API: set up with a level, step through candidates
+ * (each used for one call whose time the caller reports), pick the best, snapshot/resume.
+ *   FAST: the kernel variant only (DMMA, DFMA, and the reference kernel for
+ *          small problems), each with its automatic shape;
+ *   MEDIUM ("numerical blocking parameters of the back-transformation"):
+ *          FAST plus every compiled DMMA shape (D, CW, NCT) for this nbw.
+ * The object is host state only; it never touches the device.
+ * ------------------------------------------------------------------------------------- */
+typedef struct elpa_b200_autotune elpa_b200_autotune;
+enum { ELPA_B200_AUTOTUNE_FAST = 1, ELPA_B200_AUTOTUNE_MEDIUM = 2 };
+
+/* NULL on bad arguments (*error = ELPA_B200_ERR_ARG) */
+elpa_b200_autotune *elpa_b200_autotune_setup(int64_t n, int64_t nbw, int64_t nev, int level, int *error);
+/* 1 and the next candidate in *opts while candidates remain, 0 when all were tried, <0 error */
+int elpa_b200_autotune_step(elpa_b200_autotune *at, elpa_b200_opts *opts);
+/* time (ms, > 0) of the candidate the last _step returned */
+int elpa_b200_autotune_report(elpa_b200_autotune *at, double ms);
+/* best candidate reported so far (ELPA_B200_ERR_ARG if none) */
+int elpa_b200_autotune_best(const elpa_b200_autotune *at, elpa_b200_opts *opts, double *ms);
+/* number of candidates, and how many were reported */
+int elpa_b200_autotune_progress(const elpa_b200_autotune *at, int *tried, int *total);
+/* snapshot: writes a text state into buf; returns its length (incl. NUL) or the
+ * size needed when buflen is too small; resume with _load */
+int64_t elpa_b200_autotune_save(const elpa_b200_autotune *at, char *buf, size_t buflen);
+elpa_b200_autotune *elpa_b200_autotune_load(const char *state, int *error);
+void elpa_b200_autotune_destroy(elpa_b200_autotune *at);
+/* Convenience: run the whole loop on device buffers.  Prepares the reflectors once per kernel
+ * variant, times each candidate's apply on Q (which is overwritten: pass a scratch copy) with
+ * CUDA events on `stream` (best of `reps`), returns the best options and time. */
+int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+                           double *Q_scratch, int64_t ldq, elpa_b200_stream_t stream, int level, int reps,
+                           elpa_b200_opts *best, double *best_ms);
+
 /* Static description of an error code. */
 const char *elpa_b200_strerror(int code);
 

@@ -41,6 +41,25 @@ def _load():
     lib.elpa_b200_describe.argtypes = [i64, i64, i64, p, ctypes.c_char_p, sz]
     lib.elpa_b200_strerror.restype = ctypes.c_char_p
     lib.elpa_b200_strerror.argtypes = [i32]
+    pi = ctypes.POINTER(ctypes.c_int)
+    lib.elpa_b200_autotune_setup.restype = p
+    lib.elpa_b200_autotune_setup.argtypes = [i64, i64, i64, i32, pi]
+    lib.elpa_b200_autotune_step.restype = i32
+    lib.elpa_b200_autotune_step.argtypes = [p, p]
+    lib.elpa_b200_autotune_report.restype = i32
+    lib.elpa_b200_autotune_report.argtypes = [p, ctypes.c_double]
+    lib.elpa_b200_autotune_best.restype = i32
+    lib.elpa_b200_autotune_best.argtypes = [p, p, ctypes.POINTER(ctypes.c_double)]
+    lib.elpa_b200_autotune_progress.restype = i32
+    lib.elpa_b200_autotune_progress.argtypes = [p, pi, pi]
+    lib.elpa_b200_autotune_save.restype = i64
+    lib.elpa_b200_autotune_save.argtypes = [p, ctypes.c_char_p, sz]
+    lib.elpa_b200_autotune_load.restype = p
+    lib.elpa_b200_autotune_load.argtypes = [ctypes.c_char_p, pi]
+    lib.elpa_b200_autotune_destroy.restype = None
+    lib.elpa_b200_autotune_destroy.argtypes = [p]
+    lib.elpa_b200_autotune_run.restype = i32
+    lib.elpa_b200_autotune_run.argtypes = [i64, i64, i64, p, p, p, i64, p, i32, i32, p, ctypes.POINTER(ctypes.c_double)]
     return lib
 
 
@@ -177,3 +196,82 @@ def describe(n, nbw, nev, opts=None):
 def credited_flops(n, nbw, nev):
     """North-star flop credit: 4 * nbw * nev per reflector (BASELINE.json metric)."""
     return 4.0 * nbw * nev * hh_count(n, nbw)
+
+
+AUTOTUNE_FAST, AUTOTUNE_MEDIUM = 1, 2
+
+
+def opts_dict(o):
+    return {f: getattr(o, f) for f, _ in Opts._fields_}
+
+
+class Autotuner:
+    """ELPA-style autotuning of the back-transformation's blocking parameters:
+
+        at = Autotuner(n, nbw, nev, AUTOTUNE_MEDIUM)
+        while (opts := at.step()) is not None:
+            ... run one trans_ev_tridi_to_band(..., opts=opts), time it ...
+            at.report(ms)
+        best_opts, best_ms = at.best()
+
+    save() / Autotuner.load(state) snapshot and resume the loop."""
+
+    def __init__(self, n=None, nbw=None, nev=None, level=AUTOTUNE_FAST, _handle=None):
+        if _handle is None:
+            err = ctypes.c_int(0)
+            _handle = _lib.elpa_b200_autotune_setup(int(n), int(nbw), int(nev), int(level), ctypes.byref(err))
+            if not _handle:
+                raise ElpaB200Error(err.value, "elpa_b200_autotune_setup")
+        self._h = ctypes.c_void_p(_handle)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.elpa_b200_autotune_destroy(self._h)
+            self._h = None
+
+    def step(self):
+        o = Opts()
+        rc = _lib.elpa_b200_autotune_step(self._h, ctypes.byref(o))
+        if rc < 0:
+            raise ElpaB200Error(rc, "elpa_b200_autotune_step")
+        return opts_dict(o) if rc == 1 else None
+
+    def report(self, ms):
+        _check(_lib.elpa_b200_autotune_report(self._h, float(ms)), "elpa_b200_autotune_report")
+
+    def best(self):
+        o, ms = Opts(), ctypes.c_double(0)
+        _check(_lib.elpa_b200_autotune_best(self._h, ctypes.byref(o), ctypes.byref(ms)), "elpa_b200_autotune_best")
+        return opts_dict(o), ms.value
+
+    def progress(self):
+        a, b = ctypes.c_int(0), ctypes.c_int(0)
+        _check(_lib.elpa_b200_autotune_progress(self._h, ctypes.byref(a), ctypes.byref(b)), "progress")
+        return a.value, b.value
+
+    def save(self):
+        need = _lib.elpa_b200_autotune_save(self._h, None, 0)
+        buf = ctypes.create_string_buffer(int(need))
+        _lib.elpa_b200_autotune_save(self._h, buf, int(need))
+        return buf.value.decode()
+
+    @classmethod
+    def load(cls, state):
+        err = ctypes.c_int(0)
+        h = _lib.elpa_b200_autotune_load(state.encode(), ctypes.byref(err))
+        if not h:
+            raise ElpaB200Error(err.value or ERR_ARG, "elpa_b200_autotune_load")
+        return cls(_handle=h)
+
+
+def autotune(n, nbw, hh_v, hh_tau, Q_scratch, level=AUTOTUNE_MEDIUM, reps=2, stream=None):
+    """Run the autotuning loop on device buffers (elpa_b200_autotune_run); Q_scratch is
+    overwritten.  Returns (best opts dict, best apply time in ms)."""
+    nev, ldq = _q_ldq(Q_scratch)
+    o, ms = Opts(), ctypes.c_double(0)
+    s = _stream_handle(stream, Q_scratch.device)
+    rc = _lib.elpa_b200_autotune_run(int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v"), _dev_ptr(hh_tau, "hh_tau"),
+                                     _dev_ptr(Q_scratch, "Q"), int(ldq), s, int(level), int(reps), ctypes.byref(o),
+                                     ctypes.byref(ms))
+    _check(rc, "elpa_b200_autotune_run")
+    return opts_dict(o), ms.value

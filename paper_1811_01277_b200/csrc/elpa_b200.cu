@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "../../include/elpa_b200.h"
@@ -497,6 +498,216 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     if (hs) cudaStreamDestroy(hs);
     if (ds) cudaStreamDestroy(ds);
     if (rc != ELPA_B200_OK) cudaGetLastError();
+    return rc;
+}
+
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------
+// Autotuning (header: elpa_b200_autotune_*).  Host-side state machine over candidate options.
+// ------------------------------------------------------------------------------------------
+struct elpa_b200_autotune {
+    int64_t n = 0, nbw = 0, nev = 0;
+    int level = 0;
+    std::vector<elpa_b200_opts> cand;
+    std::vector<double> ms;       // reported time per candidate (< 0: not yet)
+    int next = 0;                 // index the next _step returns
+    int last = -1;                // index the last _step returned (awaiting _report)
+};
+
+namespace {
+std::vector<elpa_b200_opts> autotune_candidates(int64_t n, int64_t nbw, int64_t nev, int level) {
+    std::vector<elpa_b200_opts> c;
+    auto mk = [](int kernel, int D, int CW, int NCT) {
+        elpa_b200_opts o{};
+        o.kernel = kernel; o.depth_warps = D; o.col_warps = CW; o.tiles_per_warp = NCT;
+        o.groups_per_step = (D || CW || NCT) ? 1 : 0;
+        return o;
+    };
+    const bool dmma = b8_supported(nbw);
+    if (dmma) {
+        c.push_back(mk(ELPA_B200_KERNEL_DMMA, 0, 0, 0));
+        c.push_back(mk(ELPA_B200_KERNEL_DFMA, 0, 0, 0));
+    }
+    // the bit-exact reference kernel is a candidate only where it can finish quickly
+    if (!dmma || double(hh_total(n, nbw)) * double(nev) * double(nbw) < 2e9)
+        c.push_back(mk(ELPA_B200_KERNEL_REFERENCE, 0, 0, 0));
+    if (level >= ELPA_B200_AUTOTUNE_MEDIUM && dmma) {
+        const int b8 = int(nbw / 8);
+        auto add = [&](const Shape *sh, size_t cnt, int kernel) {
+            for (size_t i = 0; i < cnt; i++) {
+                elpa_b200_opts o = mk(kernel, sh[i].D, sh[i].CW, sh[i].NCT);
+                Plan p;
+                if (make_plan(n, nbw, nev, &o, p) == ELPA_B200_OK) c.push_back(o);
+            }
+        };
+        if (b8_full_menu(b8)) {
+            add(kShapes, sizeof(kShapes) / sizeof(kShapes[0]), ELPA_B200_KERNEL_DMMA);
+            add(kDfmaShapes, sizeof(kDfmaShapes) / sizeof(kDfmaShapes[0]), ELPA_B200_KERNEL_DFMA);
+        } else {
+            add(kSmallShapes, sizeof(kSmallShapes) / sizeof(kSmallShapes[0]), ELPA_B200_KERNEL_DMMA);
+        }
+    }
+    return c;
+}
+}  // namespace
+
+extern "C" {
+
+elpa_b200_autotune *elpa_b200_autotune_setup(int64_t n, int64_t nbw, int64_t nev, int level, int *error) {
+    if (error) *error = ELPA_B200_OK;
+    if (n < 0 || nbw < 1 || nev < 0 || nev > n ||
+        (level != ELPA_B200_AUTOTUNE_FAST && level != ELPA_B200_AUTOTUNE_MEDIUM)) {
+        if (error) *error = ELPA_B200_ERR_ARG;
+        return nullptr;
+    }
+    auto *at = new elpa_b200_autotune;
+    at->n = n; at->nbw = nbw; at->nev = nev; at->level = level;
+    at->cand = autotune_candidates(n, nbw, nev, level);
+    at->ms.assign(at->cand.size(), -1.0);
+    return at;
+}
+
+int elpa_b200_autotune_step(elpa_b200_autotune *at, elpa_b200_opts *opts) {
+    if (!at || !opts) return ELPA_B200_ERR_NULL;
+    if (at->next >= int(at->cand.size())) return 0;
+    at->last = at->next++;
+    *opts = at->cand[at->last];
+    return 1;
+}
+
+int elpa_b200_autotune_report(elpa_b200_autotune *at, double ms) {
+    if (!at) return ELPA_B200_ERR_NULL;
+    if (at->last < 0 || !(ms > 0.0)) return ELPA_B200_ERR_ARG;
+    at->ms[at->last] = ms;
+    at->last = -1;
+    return ELPA_B200_OK;
+}
+
+int elpa_b200_autotune_best(const elpa_b200_autotune *at, elpa_b200_opts *opts, double *ms) {
+    if (!at) return ELPA_B200_ERR_NULL;
+    int b = -1;
+    for (size_t i = 0; i < at->ms.size(); i++)
+        if (at->ms[i] > 0.0 && (b < 0 || at->ms[i] < at->ms[b])) b = int(i);
+    if (b < 0) return ELPA_B200_ERR_ARG;
+    if (opts) *opts = at->cand[b];
+    if (ms) *ms = at->ms[b];
+    return ELPA_B200_OK;
+}
+
+int elpa_b200_autotune_progress(const elpa_b200_autotune *at, int *tried, int *total) {
+    if (!at) return ELPA_B200_ERR_NULL;
+    int t = 0;
+    for (double v : at->ms) t += v > 0.0;
+    if (tried) *tried = t;
+    if (total) *total = int(at->cand.size());
+    return ELPA_B200_OK;
+}
+
+int64_t elpa_b200_autotune_save(const elpa_b200_autotune *at, char *buf, size_t buflen) {
+    if (!at) return ELPA_B200_ERR_NULL;
+    std::string st = "elpa_b200_autotune v1 " + std::to_string(at->n) + " " + std::to_string(at->nbw) + " " +
+                     std::to_string(at->nev) + " " + std::to_string(at->level) + " " + std::to_string(at->next) +
+                     " " + std::to_string(at->cand.size());
+    char tmp[64];
+    for (double v : at->ms) {
+        snprintf(tmp, sizeof tmp, " %.17g", v);
+        st += tmp;
+    }
+    const int64_t need = int64_t(st.size()) + 1;
+    if (buf && buflen >= size_t(need)) memcpy(buf, st.c_str(), size_t(need));
+    return need;
+}
+
+elpa_b200_autotune *elpa_b200_autotune_load(const char *state, int *error) {
+    if (error) *error = ELPA_B200_ERR_ARG;
+    if (!state) {
+        if (error) *error = ELPA_B200_ERR_NULL;
+        return nullptr;
+    }
+    long long n, nbw, nev;
+    int level, next, cnt, used = 0;
+    if (sscanf(state, "elpa_b200_autotune v1 %lld %lld %lld %d %d %d%n", &n, &nbw, &nev, &level, &next, &cnt,
+               &used) != 6)
+        return nullptr;
+    int err = 0;
+    elpa_b200_autotune *at = elpa_b200_autotune_setup(n, nbw, nev, level, &err);
+    if (!at) return nullptr;
+    if (int(at->cand.size()) != cnt || next < 0 || next > cnt) {   // a different build's menu
+        delete at;
+        return nullptr;
+    }
+    const char *p = state + used;
+    for (int i = 0; i < cnt; i++) {
+        int u = 0;
+        if (sscanf(p, " %lg%n", &at->ms[i], &u) != 1) {
+            delete at;
+            return nullptr;
+        }
+        p += u;
+    }
+    at->next = next;
+    if (error) *error = ELPA_B200_OK;
+    return at;
+}
+
+void elpa_b200_autotune_destroy(elpa_b200_autotune *at) { delete at; }
+
+int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+                           double *Q, int64_t ldq, elpa_b200_stream_t stream, int level, int reps,
+                           elpa_b200_opts *best, double *best_ms) {
+    int rc = validate(n, nbw, nev, hh_v, hh_tau, Q, ldq, true);
+    if (rc != ELPA_B200_OK) return rc;
+    if (!best) return ELPA_B200_ERR_NULL;
+    if (reps < 1) reps = 1;
+    int err = 0;
+    elpa_b200_autotune *at = elpa_b200_autotune_setup(n, nbw, nev, level, &err);
+    if (!at) return err;
+    if (hh_total(n, nbw) == 0 || nev == 0) {        // nothing to tune: any option is a no-op
+        elpa_b200_autotune_step(at, best);
+        if (best_ms) *best_ms = 0.0;
+        elpa_b200_autotune_destroy(at);
+        return ELPA_B200_OK;
+    }
+    if ((rc = check_device()) != ELPA_B200_OK) {
+        elpa_b200_autotune_destroy(at);
+        return rc;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) rc = fail_cuda();
+    void *ws[2] = {nullptr, nullptr};               // prepared reflectors per kernel kind
+    elpa_b200_opts o;
+    while (rc == ELPA_B200_OK && elpa_b200_autotune_step(at, &o) == 1) {
+        Plan p;
+        if ((rc = make_plan(n, nbw, nev, &o, p)) != ELPA_B200_OK) break;
+        const int kind = p.kernel == ELPA_B200_KERNEL_DFMA ? 1 : 0;
+        if (p.kernel != ELPA_B200_KERNEL_REFERENCE && !ws[kind]) {
+            if (cudaMallocAsync(&ws[kind], size_t(p.ws_bytes), s) != cudaSuccess) {
+                rc = fail_cuda();
+                break;
+            }
+            if ((rc = prepare_impl(p, n, hh_v, hh_tau, ws[kind], s)) != ELPA_B200_OK) break;
+        }
+        float bestv = 1e30f;
+        for (int r = 0; r < reps && rc == ELPA_B200_OK; r++) {
+            cudaEventRecord(e0, s);
+            rc = apply_impl(p, n, nbw, nev, hh_v, hh_tau, ws[kind], Q, ldq, s);
+            cudaEventRecord(e1, s);
+            if (rc == ELPA_B200_OK && cudaEventSynchronize(e1) != cudaSuccess) rc = fail_cuda();
+            float ms = 0.f;
+            if (rc == ELPA_B200_OK && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess && ms < bestv) bestv = ms;
+        }
+        if (rc == ELPA_B200_OK) elpa_b200_autotune_report(at, bestv > 0.f ? bestv : 1e-6);
+    }
+    for (void *w : ws)
+        if (w) cudaFreeAsync(w, s);
+    cudaStreamSynchronize(s);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (rc == ELPA_B200_OK) rc = elpa_b200_autotune_best(at, best, best_ms);
+    elpa_b200_autotune_destroy(at);
     return rc;
 }
 

@@ -309,3 +309,17 @@ def test_progress_publish_multi_column_warps(eb, shape, grid):
         got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=kernel, depth_warps=D, col_warps=CW,
                                                          tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
         assert _rel(got, want) <= TOL, kernel
+
+
+def test_autotune_run_and_use_best(eb):
+    """The one-call autotuner on device buffers returns options that run correctly."""
+    import torch
+    n, nbw, nev = 2000, 64, 600
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 8)
+    want = oracle.apply(hv, tau, s, L, Q)
+    dv, dt = torch.from_numpy(hv).cuda(), torch.from_numpy(tau).cuda()
+    scratch = torch.from_numpy(Q.copy()).cuda()
+    best, ms = eb.autotune(n, nbw, dv, dt, scratch, level=eb.AUTOTUNE_MEDIUM, reps=1)
+    assert ms > 0 and best["kernel"] in (eb.KERNEL_DMMA, eb.KERNEL_DFMA)
+    got = run_gpu(eb, n, nbw, hv, tau, Q, opts=best)
+    assert _rel(got, want) <= TOL
