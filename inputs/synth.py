@@ -100,6 +100,23 @@ def synthetic_reflectors(R, nbw, seed):
     return v, tau
 
 
+def synthetic_reflectors_torch(R, nbw, seed, device="cpu", chunk=1 << 22):
+    """torch version of synthetic_reflectors (bitwise identical), generated on `device`
+    in chunks of reflectors (C5 has 28M reflectors = 14.4 GB)."""
+    import torch
+    R, nbw = int(R), int(nbw)
+    v = torch.empty((R, nbw), dtype=torch.float64, device=device)
+    tau = torch.empty((R,), dtype=torch.float64, device=device)
+    for a in range(0, R, chunk):
+        b = min(R, a + chunk)
+        cnt = torch.arange(a * nbw, b * nbw, dtype=torch.int64, device=device)
+        blk = uniform_pm1_torch(seed ^ TAG_HHV, cnt).reshape(b - a, nbw)
+        blk[:, 0] = 1.0
+        v[a:b] = blk
+        tau[a:b] = 2.0 / (blk * blk).sum(dim=1)
+    return v, tau
+
+
 def synthetic_q_np(n, c0, c1, seed, ldq=None):
     """Columns [c0, c1) of the synthetic n x nev eigenvector block, uniform [-1,1):
     element (i, c) = stream(seed^TAG_Q)[c*n + i].  Returns (c1-c0, ldq) C-order array

@@ -323,3 +323,30 @@ def test_autotune_run_and_use_best(eb):
     assert ms > 0 and best["kernel"] in (eb.KERNEL_DMMA, eb.KERNEL_DFMA)
     got = run_gpu(eb, n, nbw, hv, tau, Q, opts=best)
     assert _rel(got, want) <= TOL
+
+
+def test_full_size_C5_sampled_columns(eb):
+    """C5 (n = 60000, nbw = 64, nev = 30000) on one GPU: 28M reflectors (14.4 GB), Q 14.4 GB,
+    byte offsets far past 2^31.  The oracle recomputes 6 sampled columns, streaming the
+    reflectors from the device in reverse-order chunks (applying chunk [r1, r2) then [r0, r1)
+    composes to the full reverse-order product)."""
+    import torch
+    from inputs import synthetic_reflectors_torch, synthetic_q_torch
+    n, nbw, nev = 60000, 64, 30000
+    seed = config_seed(5)
+    R = eb.hh_count(n, nbw)
+    dv, dt = synthetic_reflectors_torch(R, nbw, seed, device="cuda")
+    cols = [0, 7, 8, 14999, 29992, 29999]
+    Qs = torch.cat([synthetic_q_torch(n, c, c + 1, seed, device="cuda") for c in cols]).cpu().numpy()
+    dq = synthetic_q_torch(n, 0, nev, seed, device="cuda")
+    eb.trans_ev_tridi_to_band(n, nbw, dv, dt, dq)
+    torch.cuda.synchronize()
+    got = dq[cols].cpu().numpy()
+    del dq
+    s, L = oracle.schedule(n, nbw)
+    want = Qs
+    step = 1 << 22
+    for r1 in range(R, 0, -step):
+        r0 = max(0, r1 - step)
+        want = oracle.apply(dv[r0:r1].cpu().numpy(), dt[r0:r1].cpu().numpy(), s[r0:r1], L[r0:r1], want)
+    assert _rel(got, want) <= TOL

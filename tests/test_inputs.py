@@ -46,3 +46,12 @@ def test_synthetic_reflectors_recipe():
     assert np.allclose(tau * np.sum(v * v, axis=1), 2.0)
     q = synthetic_q_np(20, 0, 6, 1)
     assert np.array_equal(q[2:4], synthetic_q_np(20, 2, 4, 1))
+
+
+def test_synthetic_reflectors_torch_bitwise():
+    from inputs import synthetic_reflectors_torch
+    v, tau = synthetic_reflectors(123, 16, 9)
+    vt, taut = synthetic_reflectors_torch(123, 16, 9, chunk=50)
+    assert np.array_equal(v, vt.numpy())
+    # tau = 2/||v||^2: same value up to the summation order of the norm
+    assert np.allclose(tau, taut.numpy(), rtol=1e-15, atol=0)
