@@ -24,7 +24,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from inputs import CONFIGS, config_seed, synthetic_reflectors, synthetic_q_np, synthetic_q_torch  # noqa: E402
+from inputs import (CONFIGS, config_seed, synthetic_reflectors, synthetic_reflectors_torch,  # noqa: E402
+                    synthetic_q_np, synthetic_q_torch)
 
 METRIC = "trans_ev_tridi_to_band FP64 TFLOP/s (2*n^2*nev) and % roofline, 1/2/4/8 B200"
 UNIT = "TFLOP/s"
@@ -103,12 +104,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_rate(n, nbw, nev, seed, ncols, threads=None):
-    """Time the plain CPU oracle (oracle/, never tuned) on `ncols` sampled columns."""
+def cpu_oracle_rate(n, nbw, nev, seed, ncols, threads=None, hh=None):
+    """Time the plain CPU oracle (oracle/, never tuned) on `ncols` sampled columns.
+    hh = (hh_v, hh_tau) host arrays if already available."""
     import numpy as np
     import oracle
     s, L = oracle.schedule(n, nbw)
-    hv, tau = synthetic_reflectors(len(s), nbw, seed)
+    hv, tau = hh if hh is not None else synthetic_reflectors(len(s), nbw, seed)
     cols = np.linspace(0, nev - 1, ncols).astype(int)
     Qs = np.concatenate([synthetic_q_np(n, int(c), int(c) + 1, seed) for c in cols])
     threads = threads or os.cpu_count() or 1
@@ -174,10 +176,11 @@ def main():
 
     # ---- inputs: reflectors generated on rank 0 (host), Q shard generated on-device
     hh = torch.empty(R * (nbw + 1), dtype=torch.float64, device=dev)   # packed hh_v || hh_tau
-    if rank == 0:
-        hv_np, tau_np = synthetic_reflectors(R, nbw, seed)
-        hh[:R * nbw].copy_(torch.from_numpy(hv_np).reshape(-1))
-        hh[R * nbw:].copy_(torch.from_numpy(tau_np))
+    if rank == 0:                                 # generated on the device (C5: 14.4 GB)
+        hv_d, tau_d = synthetic_reflectors_torch(R, nbw, seed, device=dev)
+        hh[:R * nbw].copy_(hv_d.reshape(-1))
+        hh[R * nbw:].copy_(tau_d)
+        del hv_d, tau_d
     hh_v, hh_tau = hh[:R * nbw].view(R, nbw), hh[R * nbw:]
     Q = synthetic_q_torch(n, c0, c1, seed, device=dev)
     ws = torch.empty(eb.workspace_bytes(n, nbw), dtype=torch.uint8, device=dev)
@@ -233,10 +236,13 @@ def main():
         total_apps = args.warmup + args.steps
         cols = [0, nev_loc // 2, nev_loc - 1]
         s_arr, L_arr = oracle.schedule(n, nbw)
-        hv_np2, tau_np2 = synthetic_reflectors(R, nbw, seed)
         Qs = np.concatenate([synthetic_q_np(n, c0 + c, c0 + c + 1, seed) for c in cols])
+        step_r = 1 << 22                      # stream the reflectors from the device in chunks
         for _ in range(total_apps):
-            Qs = oracle.apply(hv_np2, tau_np2, s_arr, L_arr, Qs)
+            for r1 in range(R, 0, -step_r):
+                r0 = max(0, r1 - step_r)
+                Qs = oracle.apply(hh_v[r0:r1].cpu().numpy(), hh_tau[r0:r1].cpu().numpy(), s_arr[r0:r1],
+                                  L_arr[r0:r1], Qs)
         got = Q[cols].cpu().numpy()
         parity = float(np.abs(got - Qs).max() / np.abs(Qs).max())
 
@@ -286,7 +292,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r, dt, thr, nc = cpu_oracle_rate(n, nbw, nev, seed, 256)
+        r, dt, thr, nc = cpu_oracle_rate(n, nbw, nev, seed, 256 if R * nbw < 5e8 else 32,
+                                         hh=(hh_v.cpu().numpy(), hh_tau.cpu().numpy()))
         cpu = {"value": r, "unit": UNIT, "cores": thr, "kind": "oracle",
                "sample": f"{nc} evenly spaced columns of {args.config} (all {R} reflectors), {dt:.1f} s"}
 
