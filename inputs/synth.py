@@ -87,6 +87,22 @@ def band_matrix(n, nbw, seed):
     return band
 
 
+TAG_DENSE = 0x3C4D5E6F708192A3
+
+
+def dense_symmetric(n, seed):
+    """Random dense symmetric n x n matrix, entries uniform [-1,1) drawn for the lower triangle
+    column by column (c ascending, then row r >= c ascending), mirrored."""
+    n = int(n)
+    rows, cols = np.tril_indices(n)
+    order = np.lexsort((rows, cols))                 # column-major order of the lower triangle
+    vals = uniform_pm1_np(seed ^ TAG_DENSE, np.arange(len(order), dtype=np.uint64))
+    A = np.zeros((n, n))
+    A[rows[order], cols[order]] = vals
+    A = A + np.tril(A, -1).T
+    return A
+
+
 def synthetic_reflectors(R, nbw, seed):
     """Synthetic Householder reflectors for timing / sampled parity at sizes where the
     oracle's chase is too slow: v[0] = 1, v[1:] uniform [-1,1),

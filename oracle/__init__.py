@@ -50,6 +50,10 @@ def _load():
         lib.oracle_chase.argtypes = [i64, i64, p, p, p, p, p, p, p]
         lib.oracle_apply.restype = None
         lib.oracle_apply.argtypes = [i64, i64, i64, i64, p, p, p, p, p, i64, ctypes.c_int]
+        lib.oracle_reduce_to_band.restype = i64
+        lib.oracle_reduce_to_band.argtypes = [i64, i64, p, p, p, p]
+        lib.oracle_apply_full.restype = None
+        lib.oracle_apply_full.argtypes = [i64, i64, p, i64, p, p, p, i64, i64, ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -164,3 +168,54 @@ def residual(band, Q, lam):
         BX[:-dd] += bd * X[dd:]
     nrmB = np.sqrt(np.sum(band[0] ** 2) + 2.0 * np.sum(band[1:] ** 2))
     return float(np.linalg.norm(BX - X * lam[None, :]) / (n * nrmB))
+
+
+# ------------------------------------------------------------------ stage 1 (NEXT-1)
+def reduce_to_band(A, nbw):
+    """Full symmetric A (n x n) -> band (half-bandwidth nbw), one reflector per column
+    (oracle.c:oracle_reduce_to_band).  Returns (band lower storage
+    (nbw+1, n), V (K, n) rows = reflector vectors (zeros before s, v[s] = 1), tau (K,), s (K,),
+    the reduced full matrix)."""
+    lib = _load()
+    A = np.array(A, dtype=np.float64, order="F", copy=True)
+    n = A.shape[0]
+    K = max(n - nbw - 1, 0)
+    V = np.zeros((max(K, 1), n), dtype=np.float64)
+    tau = np.zeros(max(K, 1))
+    s = np.zeros(max(K, 1), dtype=np.int64)
+    k = lib.oracle_reduce_to_band(n, nbw, A.ctypes.data_as(ctypes.c_void_p), _ptr(V), _ptr(tau), _ptr(s))
+    assert k == K
+    band = np.zeros((nbw + 1, n))
+    for dd in range(nbw + 1):
+        band[dd, :n - dd] = np.diagonal(A, -dd)
+    return band, V[:K], tau[:K], s[:K], A
+
+
+def apply_full(V, tau, s, Q, n, nthreads=None):
+    """Q (nev, ldq) -> H_0 ... H_{K-1} Q for the stage-1 reflectors (oracle_apply_full)."""
+    lib = _load()
+    Q = np.array(Q, dtype=np.float64, order="C", copy=True)
+    nev, ldq = Q.shape
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    K = V.shape[0] if V.ndim == 2 else 0
+    if K and nev:
+        lib.oracle_apply_full(n, K, _ptr(V), V.shape[1], _ptr(np.ascontiguousarray(tau, dtype=np.float64)),
+                              _ptr(np.ascontiguousarray(s, dtype=np.int64)), _ptr(Q), ldq, nev,
+                              int(nthreads or os.cpu_count() or 1))
+    return Q
+
+
+def make_case_full(n, nbw, nev, seed):
+    """The whole two-stage pipeline on a random dense symmetric A (inputs.dense_symmetric):
+    A -> band (stage 1) -> tridiagonal (stage 2 chase) -> lowest nev eigenpairs of T ->
+    back-transformed twice.  Returns a dict with every intermediate."""
+    from inputs import dense_symmetric
+    A = dense_symmetric(n, seed)
+    band, V1, tau1, s1, _ = reduce_to_band(A, nbw)
+    hh_v, hh_tau, s2, L2, d, e = chase(band)
+    lam, Vhat = tridiag_eig(d, e, nev)
+    Qin = np.ascontiguousarray(Vhat.T)
+    Qband = apply(hh_v, hh_tau, s2, L2, Qin)
+    Qfull = apply_full(V1, tau1, s1, Qband, n)
+    return dict(A=A, band=band, V1=V1, tau1=tau1, s1=s1, hh_v=hh_v, hh_tau=hh_tau, s2=s2, L2=L2, d=d, e=e,
+                lam=lam, Qin=Qin, Qband=Qband, Qfull=Qfull)

@@ -214,3 +214,73 @@ void oracle_apply(int64_t n, int64_t nbw, int64_t nev, int64_t R,
         }
     }
 }
+
+/* ====================================================================================
+ * Stage 1 (NEXT-1): full -> band reduction and the band -> full back-transformation.
+ * PAPER.md P:141-143 ("the matrix is reduced to a banded form ... BLAS level 3") and
+ * P:144-146 (each eigenvector is transformed twice).  The oracle uses the unblocked form:
+ * one reflector per column; ELPA's BLAS-3 panels regroup exactly these reflectors.
+ * Reflector j (j = 0 .. n-b-2) annihilates A[j+b+1 : n, j]; it acts on rows [s, n) with
+ * s = j + b, L = n - s >= 2.  V is n x K column-major (column j = reflector j, v[s] = 1,
+ * zeros above s), K = n - b - 1 (0 if n < b + 2).
+ * ==================================================================================== */
+int64_t oracle_reduce_to_band(int64_t n, int64_t b, double *A, double *V, double *tau, int64_t *s_out) {
+    int64_t K = (n >= b + 2) ? n - b - 1 : 0;
+    double *x = (double *)malloc(sizeof(double) * (size_t)(n + 1));
+    double *v = (double *)malloc(sizeof(double) * (size_t)(n + 1));
+    for (int64_t j = 0; j < K; j++) {
+        int64_t s = j + b, L = n - s;
+        for (int64_t i = 0; i < L; i++) x[i] = A[j * n + s + i];
+        double t, beta;
+        plain_dlarfg(L, x, v, &t, &beta);
+        if (t != 0.0) {
+            /* left: A[s:, c] <- H A[s:, c] for all columns c */
+            for (int64_t c = 0; c < n; c++) {
+                double p = 0.0;
+                for (int64_t i = 0; i < L; i++) p += v[i] * A[c * n + s + i];
+                p *= t;
+                for (int64_t i = 0; i < L; i++) A[c * n + s + i] -= p * v[i];
+            }
+            /* right: A[r, s:] <- A[r, s:] H for all rows r */
+            for (int64_t r = 0; r < n; r++) {
+                double q = 0.0;
+                for (int64_t i = 0; i < L; i++) q += A[(s + i) * n + r] * v[i];
+                q *= t;
+                for (int64_t i = 0; i < L; i++) A[(s + i) * n + r] -= q * v[i];
+            }
+        }
+        /* eliminated column/row: exactly (beta, 0, ..., 0) */
+        A[j * n + s] = beta;
+        A[s * n + j] = beta;
+        for (int64_t i = 1; i < L; i++) {
+            A[j * n + s + i] = 0.0;
+            A[(s + i) * n + j] = 0.0;
+        }
+        for (int64_t i = 0; i < n; i++) V[j * n + i] = (i < s) ? 0.0 : v[i - s];
+        tau[j] = t;
+        s_out[j] = s;
+    }
+    free(x);
+    free(v);
+    return K;
+}
+
+/* Q_out = H_0 H_1 ... H_{K-1} Q (reflector K-1 applied first), H_r = I - tau_r v_r v_r^T on rows
+ * [s_r, n): for r = K-1 .. 0, per column: w = tau_r * sum_{i>=s_r} v_r[i] Q[i] (v_r[s_r] = 1,
+ * increasing i), Q[i] -= w v_r[i].  V: n x K column-major (ldv), Q: nev x ldq (row c = column c). */
+void oracle_apply_full(int64_t n, int64_t K, const double *V, int64_t ldv, const double *tau, const int64_t *s_arr,
+                       double *Q, int64_t ldq, int64_t nev, int nthreads) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t c = 0; c < nev; c++) {
+        double *q = Q + c * ldq;
+        for (int64_t r = K - 1; r >= 0; r--) {
+            const double *v = V + r * ldv;
+            int64_t s = s_arr[r];
+            double sum = q[s];                          /* v[s] == 1 */
+            for (int64_t i = s + 1; i < n; i++) sum += v[i] * q[i];
+            double w = tau[r] * sum;
+            q[s] -= w;
+            for (int64_t i = s + 1; i < n; i++) q[i] -= w * v[i];
+        }
+    }
+}
