@@ -174,6 +174,22 @@ int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh
                            double *Q_scratch, int64_t ldq, elpa_b200_stream_t stream, int level, int reps,
                            elpa_b200_opts *best, double *best_ms);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-1: band -> full back-transformation (the second transform of every eigenvector in the
+ * two-stage solver).  Stage-1 reflector j (j = 0 .. K-1) annihilated column j of the
+ * full -> band reduction below row j + nbw; it acts on rows [j + nbw, n):
+ *      Q <- H_0 H_1 ... H_{K-1} Q        (H_{K-1} applied first), K = n - nbw - 1.
+ * hh1_v  : device, n x K column-major (ldv >= n); column j = reflector j; the element at row
+ *          j + nbw is treated as 1.0 and rows above it are never read.
+ * hh1_tau: device, K doubles (0 = identity).
+ * Q      : device, n x nev column-major (ldq >= n), updated in place.
+ * Blocked compact WY (panels of 128 reflectors) with FP64-tensor-core DGEMMs (cuBLAS, loaded at
+ * run time: ELPA_B200_ERR_CUDA if it cannot be loaded).  Asynchronous on `stream`.
+ * ------------------------------------------------------------------------------------- */
+int64_t elpa_b2f_count(int64_t n, int64_t nbw);   /* K, or -1 on bad arguments */
+int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double *hh1_v, int64_t ldv,
+                               const double *hh1_tau, double *Q, int64_t ldq, elpa_b200_stream_t stream);
+
 /* Static description of an error code. */
 const char *elpa_b200_strerror(int code);
 

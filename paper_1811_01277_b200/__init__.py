@@ -58,6 +58,10 @@ def _load():
     lib.elpa_b200_autotune_load.argtypes = [ctypes.c_char_p, pi]
     lib.elpa_b200_autotune_destroy.restype = None
     lib.elpa_b200_autotune_destroy.argtypes = [p]
+    lib.elpa_b2f_count.restype = i64
+    lib.elpa_b2f_count.argtypes = [i64, i64]
+    lib.elpa_trans_ev_band_to_full.restype = i32
+    lib.elpa_trans_ev_band_to_full.argtypes = [i64, i64, i64, p, i64, p, p, i64, p]
     lib.elpa_b200_autotune_run.restype = i32
     lib.elpa_b200_autotune_run.argtypes = [i64, i64, i64, p, p, p, i64, p, i32, i32, p, ctypes.POINTER(ctypes.c_double)]
     return lib
@@ -275,3 +279,23 @@ def autotune(n, nbw, hh_v, hh_tau, Q_scratch, level=AUTOTUNE_MEDIUM, reps=2, str
                                      ctypes.byref(ms))
     _check(rc, "elpa_b200_autotune_run")
     return opts_dict(o), ms.value
+
+
+def b2f_count(n, nbw):
+    """K = number of stage-1 reflectors of an n x n matrix reduced to half-bandwidth nbw."""
+    return int(_lib.elpa_b2f_count(int(n), int(nbw)))
+
+
+def trans_ev_band_to_full(n, nbw, hh1_v, hh1_tau, Q, stream=None):
+    """NEXT-1: Q <- H_0 ... H_{K-1} Q with the stage-1 (full -> band) reflectors
+    (elpa_trans_ev_band_to_full).  hh1_v: (K, ldv) float64 CUDA tensor (row j = reflector j's
+    length-n column, the element at j + nbw treated as 1, earlier ones ignored); hh1_tau: (K,)."""
+    nev, ldq = _q_ldq(Q)
+    if hh1_v.dim() != 2 or hh1_v.stride(1) != 1:
+        raise ValueError("hh1_v must be a (K, ldv) tensor with unit inner stride")
+    ldv = hh1_v.stride(0) if hh1_v.shape[0] > 1 else max(hh1_v.shape[1], int(n))
+    s = _stream_handle(stream, Q.device)
+    rc = _lib.elpa_trans_ev_band_to_full(int(n), int(nbw), int(nev), _dev_ptr(hh1_v, "hh1_v"), int(ldv),
+                                         _dev_ptr(hh1_tau, "hh1_tau"), _dev_ptr(Q, "Q"), int(ldq), s)
+    _check(rc, "elpa_trans_ev_band_to_full")
+    return Q

@@ -104,3 +104,12 @@ def test_describe_and_workspace():
     groups = sum(G0 - m * b8 for m in range(M))
     assert eb.workspace_bytes(n, b) == groups * 128 * lam * 8
     assert eb.workspace_bytes(100, 6) == 0
+
+
+def test_b2f_count_and_validation():
+    assert eb.b2f_count(20, 4) == 15 and eb.b2f_count(5, 4) == 0 and eb.b2f_count(-1, 4) == -1
+    lib = eb._lib
+    assert lib.elpa_trans_ev_band_to_full(10, 0, 5, FAKE, 10, FAKE, FAKE, 10, None) == eb.ERR_ARG
+    assert lib.elpa_trans_ev_band_to_full(10, 2, 5, FAKE, 9, FAKE, FAKE, 10, None) == eb.ERR_ARG   # ldv < n
+    assert lib.elpa_trans_ev_band_to_full(10, 2, 5, None, 10, FAKE, FAKE, 10, None) == eb.ERR_NULL
+    assert lib.elpa_trans_ev_band_to_full(4, 3, 2, None, 4, None, None, 4, None) == eb.OK          # K = 0

@@ -350,3 +350,36 @@ def test_full_size_C5_sampled_columns(eb):
         r0 = max(0, r1 - step)
         want = oracle.apply(dv[r0:r1].cpu().numpy(), dt[r0:r1].cpu().numpy(), s[r0:r1], L[r0:r1], want)
     assert _rel(got, want) <= TOL
+
+
+# ------------------------------------------------------------------ NEXT-1: band -> full
+@pytest.mark.parametrize("n,nbw,nev", [(300, 16, 40), (517, 64, 101), (200, 1, 33), (130, 128, 7), (1000, 32, 400)])
+def test_band_to_full_vs_oracle(eb, n, nbw, nev):
+    import torch
+    from inputs import dense_symmetric
+    A = dense_symmetric(n, n + nbw)
+    band, V, tau, s1, _ = oracle.reduce_to_band(A, nbw)
+    Q = synthetic_q_np(n, 0, nev, 9, ldq=n + (n & 1))
+    want = oracle.apply_full(V, tau, s1, Q, n)
+    dq = torch.from_numpy(Q.copy()).cuda()
+    eb.trans_ev_band_to_full(n, nbw, torch.from_numpy(V).cuda(), torch.from_numpy(tau).cuda(), dq)
+    torch.cuda.synchronize()
+    got = dq.cpu().numpy()
+    assert _rel(got[:, :n], want[:, :n]) <= TOL
+    assert np.array_equal(got[:, n:], Q[:, n:])
+
+
+@pytest.mark.parametrize("n,nbw,nev", [(512, 16, 512), (1200, 64, 300)])
+def test_two_stage_pipeline_on_gpu(eb, n, nbw, nev):
+    """The whole ELPA-2 eigenvector back-transformation on the GPU: tridiagonal
+    eigenvectors -> band (DMMA kernel) -> full (NEXT-1); residual against the dense A."""
+    import torch
+    c = oracle.make_case_full(n, nbw, nev, 5 + n)
+    dq = torch.from_numpy(c["Qin"].copy()).cuda()
+    eb.trans_ev_tridi_to_band(n, nbw, torch.from_numpy(c["hh_v"]).cuda(), torch.from_numpy(c["hh_tau"]).cuda(), dq)
+    eb.trans_ev_band_to_full(n, nbw, torch.from_numpy(c["V1"]).cuda(), torch.from_numpy(c["tau1"]).cuda(), dq)
+    torch.cuda.synchronize()
+    got = dq.cpu().numpy()
+    assert _rel(got, c["Qfull"]) <= TOL
+    A, X, lam = c["A"], got.T, c["lam"]
+    assert np.linalg.norm(A @ X - X * lam) / (n * np.linalg.norm(A)) <= 1e-13
