@@ -785,8 +785,15 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
     double *T = reinterpret_cast<double *>(buf + up(bV) + up(bG));
     double *W = reinterpret_cast<double *>(buf + up(bV) + 2 * up(bG)), *W2 = reinterpret_cast<double *>(
                                                                               buf + up(bV) + 2 * up(bG) + up(bW));
-    cublas_handle_t h = nullptr;
-    if (cb.create(&h) != 0 || cb.set_stream(h, s) != 0) rc = ELPA_B200_ERR_CUDA;
+    // one cuBLAS handle per host thread and device, created on first use (handle creation
+    // costs milliseconds; the handle carries no problem state, the stream is set per call)
+    thread_local cublas_handle_t handles[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cublas_handle_t h = (dev >= 0 && dev < 64) ? handles[dev] : nullptr;
+    if (!h && cb.create(&h) != 0) h = nullptr;
+    if (h && dev >= 0 && dev < 64) handles[dev] = h;
+    if (!h || cb.set_stream(h, s) != 0) rc = ELPA_B200_ERR_CUDA;
     const double one = 1.0, zero = 0.0, mone = -1.0;
     if (rc == ELPA_B200_OK) {
         dim3 g(unsigned(std::min<int64_t>(1024, (n * P + 255) / 256)), unsigned(np));
@@ -814,7 +821,7 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
             cb.dgemm(h, kOpN, kOpN, int(m), int(nev), int(P), &mone, vp, int(m), W2, int(P), &one, q, int(ldq)) != 0)
             rc = ELPA_B200_ERR_CUDA;
     }
-    if (h) cb.destroy(h);
+    if (h && !(dev >= 0 && dev < 64)) cb.destroy(h);
     if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
     if (rc != ELPA_B200_OK) cudaGetLastError();
     return rc;
