@@ -58,7 +58,8 @@ enum {
     ELPA_B200_OK = 0,
     ELPA_B200_ERR_ARG = -1,    /* n < 0, nbw < 1, nev < 0, nev > n, ldq < max(1,n), bad opts */
     ELPA_B200_ERR_NULL = -2,   /* a required pointer is NULL (R > 0 and nev > 0) */
-    ELPA_B200_ERR_ALIGN = -3,  /* ldq odd or Q not 16-byte aligned; workspace not 256-byte aligned */
+    ELPA_B200_ERR_ALIGN = -3,  /* Q not 16-byte aligned, ldq odd (FP64) / not a multiple of 4 (FP32);
+                                  workspace not 256-byte aligned */
     ELPA_B200_ERR_DEVICE = -4, /* current device is not compute capability 10.0 (B200, sm_100a) */
     ELPA_B200_ERR_CUDA = -5,   /* a CUDA runtime call or kernel launch failed */
     ELPA_B200_ERR_SPACE = -6   /* workspace smaller than elpa_b200_workspace_bytes() */
@@ -72,8 +73,10 @@ enum {
     ELPA_B200_KERNEL_DMMA = 2,      /* k = 8 compact-WY groups on FP64 tensor cores (DMMA),
                                        depth-pipelined row windows; nbw % 8 == 0, nbw <= 128
                                        (AUTO picks it then, else REFERENCE) */
-    ELPA_B200_KERNEL_DFMA = 3       /* the same groups and schedule on FP64 CUDA cores (DFMA +
+    ELPA_B200_KERNEL_DFMA = 3,      /* the same groups and schedule on FP64 CUDA cores (DFMA +
                                        warp shuffles): the measured alternative to DMMA */
+    ELPA_B200_KERNEL_FFMA2 = 4      /* FP32 entry point only: packed FP32 FMA (f32x2) kernel,
+                                       same schedule; nbw % 8 == 0, nbw <= 128 */
 };
 
 /* Optional tuning knobs (the paper's "numerical blocking parameters of the
@@ -189,6 +192,26 @@ int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh
 int64_t elpa_b2f_count(int64_t n, int64_t nbw);   /* K, or -1 on bad arguments */
 int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double *hh1_v, int64_t ldv,
                                const double *hh1_tau, double *Q, int64_t ldq, elpa_b200_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3: FP32 variant.  ELPA offers the whole solver in single precision, and
+ * single precision in the eigen-steps is where the paper's 1.3-1.5x SCF gains come from
+ * (P:663-692).  Same operation, reflector order, storage conventions, validation order and
+ * error codes as elpa_trans_ev_tridi_to_band, on float data:
+ *   hh_v   : device, nbw x R floats; hh_tau: device, R floats;
+ *   Q      : device, n x nev floats, ldq % 4 == 0 and Q 16-byte aligned (else ERR_ALIGN).
+ * opts (may be NULL): kernel AUTO (FFMA2 when nbw % 8 == 0 and nbw <= 128, else REFERENCE),
+ *   ELPA_B200_KERNEL_FFMA2 or ELPA_B200_KERNEL_REFERENCE (one thread per column, explicitly
+ *   rounded FP32, any nbw); depth_warps = D, col_warps = CW, tiles_per_warp = NC (32-column
+ *   blocks per warp, 1 or 2), grid_ctas as for FP64; groups_per_step must be 0 or 1.
+ * Accuracy: FP32 rounding, tolerance DESIGN.md R14.  Asynchronous on `stream`; the temporary
+ * workspace comes from cudaMallocAsync/cudaFreeAsync on `stream`.
+ * ------------------------------------------------------------------------------------- */
+int elpa_trans_ev_tridi_to_band_f32(int64_t n, int64_t nbw, int64_t nev, const float *hh_v, const float *hh_tau,
+                                    float *Q, int64_t ldq, elpa_b200_stream_t stream, const elpa_b200_opts *opts);
+/* As elpa_b200_describe, for the FP32 entry point. */
+int elpa_b200_describe_f32(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *opts,
+                           char *buf, size_t buflen);
 
 /* Static description of an error code. */
 const char *elpa_b200_strerror(int code);

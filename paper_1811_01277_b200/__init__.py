@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libelpa_b200.so")
 
 OK, ERR_ARG, ERR_NULL, ERR_ALIGN, ERR_DEVICE, ERR_CUDA, ERR_SPACE = 0, -1, -2, -3, -4, -5, -6
-KERNEL_AUTO, KERNEL_REFERENCE, KERNEL_DMMA, KERNEL_DFMA = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_REFERENCE, KERNEL_DMMA, KERNEL_DFMA, KERNEL_FFMA2 = 0, 1, 2, 3, 4
 
 
 def _load():
@@ -31,6 +31,10 @@ def _load():
     for f in (lib.elpa_trans_ev_tridi_to_band_ex, lib.elpa_trans_ev_tridi_to_band_host):
         f.restype = i32
         f.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
+    lib.elpa_trans_ev_tridi_to_band_f32.restype = i32
+    lib.elpa_trans_ev_tridi_to_band_f32.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
+    lib.elpa_b200_describe_f32.restype = i32
+    lib.elpa_b200_describe_f32.argtypes = [i64, i64, i64, p, ctypes.c_char_p, sz]
     lib.elpa_b200_workspace_bytes.restype = i64
     lib.elpa_b200_workspace_bytes.argtypes = [i64, i64, p]
     lib.elpa_b200_prepare.restype = i32
@@ -112,12 +116,13 @@ def _check(rc, where):
         raise ElpaB200Error(rc, where)
 
 
-def _dev_ptr(t, name):
+def _dev_ptr(t, name, dtype=None):
     import torch
     if t is None:
         return None
-    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
-        raise TypeError(f"{name} must be a float64 CUDA tensor")
+    dtype = dtype or torch.float64
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or not t.is_cuda:
+        raise TypeError(f"{name} must be a {str(dtype).replace('torch.', '')} CUDA tensor")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -129,10 +134,19 @@ def _q_ldq(Q):
 
 def trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Q, stream=None, opts=None):
     """Q <- H_0 H_1 ... H_{R-1} Q in place on the GPU (elpa_trans_ev_tridi_to_band[_ex]).
-    Asynchronous on `stream` (default: torch's current stream)."""
+    Asynchronous on `stream` (default: torch's current stream).  float32 tensors go to the
+    FP32 variant (elpa_trans_ev_tridi_to_band_f32, NEXT-3); all three must share the dtype."""
+    import torch
     nev, ldq = _q_ldq(Q)
     o, op = _opts_ptr(opts)
     s = _stream_handle(stream, Q.device)
+    if isinstance(Q, torch.Tensor) and Q.dtype == torch.float32:
+        f = torch.float32
+        rc = _lib.elpa_trans_ev_tridi_to_band_f32(int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v", f),
+                                                  _dev_ptr(hh_tau, "hh_tau", f), _dev_ptr(Q, "Q", f), int(ldq), s,
+                                                  op)
+        _check(rc, "elpa_trans_ev_tridi_to_band_f32")
+        return Q
     args = (int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v"), _dev_ptr(hh_tau, "hh_tau"),
             _dev_ptr(Q, "Q"), int(ldq), s)
     rc = _lib.elpa_trans_ev_tridi_to_band(*args) if op is None else \
@@ -185,6 +199,16 @@ def apply_prepared(n, nbw, workspace, Q, hh_v=None, hh_tau=None, stream=None, op
                                        int(ldq), s, op)
     _check(rc, "elpa_b200_apply_prepared")
     return Q
+
+
+def describe_f32(n, nbw, nev, opts=None):
+    """(launches, description) of the FP32 entry point's plan (elpa_b200_describe_f32)."""
+    o, op = _opts_ptr(opts)
+    buf = ctypes.create_string_buffer(512)
+    rc = _lib.elpa_b200_describe_f32(int(n), int(nbw), int(nev), op, buf, 512)
+    if rc < 0:
+        raise ElpaB200Error(rc, "elpa_b200_describe_f32")
+    return rc, buf.value.decode()
 
 
 def describe(n, nbw, nev, opts=None):

@@ -1,20 +1,23 @@
-"""Build the C-ABI library libelpa_b200.so in-tree (sm_100a SASS only, static cudart)."""
+"""Build the C-ABI library libelpa_b200.so in-tree (sm_100a SASS only, static cudart).
+The translation units (FP64 path, FP32 path) compile in parallel, then link."""
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libelpa_b200.so")
-SOURCES = [os.path.join(CSRC, "elpa_b200.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + \
+SOURCES = [os.path.join(CSRC, "elpa_b200.cu"), os.path.join(CSRC, "elpa_b200_f32.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
     [os.path.join(ROOT, "include", "elpa_b200.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC,-O2", "-shared", "-cudart", "static", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-ldl"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+                 "-I", os.path.join(ROOT, "include")]
+LFLAGS = ARCH + ["-shared", "-cudart", "static", "-ldl"]
 
 
 def stale():
@@ -24,16 +27,31 @@ def stale():
     return any(os.path.getmtime(f) > t for f in DEPS)
 
 
+def _run(cmd):
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
 def build(force=False, verbose=False):
     if not force and not stale():
         return SO
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", SO] + SOURCES
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objs = [os.path.join(CSRC, os.path.basename(s)[:-3] + ".o") for s in SOURCES]
+    cmds = [[NVCC] + CFLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", "-o", o, s]
+            for s, o in zip(SOURCES, objs)]
+    with ThreadPoolExecutor(len(cmds)) as ex:
+        results = list(ex.map(_run, cmds))
+    for r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libelpa_b200.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    r = _run([NVCC] + LFLAGS + ["-o", SO] + objs)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libelpa_b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libelpa_b200.so")
     return SO
 
 

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/elpa_b200.h"
+#include "host_common.h"
 #include "geometry.cuh"
 #include "kernel_dmma.cuh"
 #include "kernel_prep.cuh"
@@ -20,10 +21,9 @@
 #include <dlfcn.h>
 
 using namespace elpa_b200;
+using namespace elpa_b200_host;
 
 namespace {
-
-constexpr int kMaxSms = 148;
 
 struct Plan {
     int kernel = ELPA_B200_KERNEL_REFERENCE;
@@ -36,39 +36,6 @@ struct Plan {
     size_t smem = 0;
     int64_t ws_bytes = 0;
 };
-
-int sm_count() {
-    int dev = 0, n = kMaxSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
-    return n > 0 ? n : kMaxSms;
-}
-
-// A failed runtime call leaves a "last error" that a later cudaGetLastError() after a
-// successful launch would report; clear it so every call reports only its own failures.
-int fail_cuda() {
-    cudaGetLastError();
-    return ELPA_B200_ERR_CUDA;
-}
-
-// Progress-publish period in steps: each publish is a release fence on the
-// CTA's critical path, but a next pass chained right behind waits for it.  Development
-// override: ELPA_B200_PUB.
-int pub_period() {
-    static int v = [] {
-        const char *e = getenv("ELPA_B200_PUB");
-        int x = e ? atoi(e) : 32;
-        return x >= 1 ? x : 32;
-    }();
-    return v;
-}
-
-int smem_optin() {
-    int dev = 0, v = 232448;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaGetLastError();   // no device (CPU host): keep the B200 value, clear the error
-    return v > 0 ? v : 232448;
-}
 
 // nbw = 8*b8 with b8 in 1..16 runs on the DMMA path; {1,2,4,8} (nbw 8/16/32/64) get the full
 // shape menu, the other multiples of 8 up to 128 a small one (compile-time budget)
@@ -174,15 +141,6 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;   // shape does not fit this nbw
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1, kernel == ELPA_B200_KERNEL_DFMA) * 8 : 0;
     return ELPA_B200_OK;
-}
-
-int check_device() {
-    int dev = 0, major = 0, minor = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return ELPA_B200_ERR_DEVICE;
-    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
-        return ELPA_B200_ERR_DEVICE;
-    return (major == 10 && minor == 0) ? ELPA_B200_OK : ELPA_B200_ERR_DEVICE;
 }
 
 int validate(int64_t n, int64_t nbw, int64_t nev, const void *hh_v, const void *hh_tau, const void *Q,
@@ -322,7 +280,7 @@ const char *elpa_b200_strerror(int code) {
         case ELPA_B200_OK: return "ok";
         case ELPA_B200_ERR_ARG: return "invalid argument (n, nbw, nev, ldq or options)";
         case ELPA_B200_ERR_NULL: return "required pointer is NULL";
-        case ELPA_B200_ERR_ALIGN: return "misaligned Q (ldq must be even, Q 16-byte aligned) or workspace";
+        case ELPA_B200_ERR_ALIGN: return "misaligned Q (FP64: ldq even; FP32: ldq % 4 == 0; Q 16-byte aligned) or workspace";
         case ELPA_B200_ERR_DEVICE: return "current device is not an sm_100 (B200) GPU";
         case ELPA_B200_ERR_CUDA: return "CUDA runtime error or kernel launch failure";
         case ELPA_B200_ERR_SPACE: return "workspace too small";

@@ -113,3 +113,43 @@ def test_b2f_count_and_validation():
     assert lib.elpa_trans_ev_band_to_full(10, 2, 5, FAKE, 9, FAKE, FAKE, 10, None) == eb.ERR_ARG   # ldv < n
     assert lib.elpa_trans_ev_band_to_full(10, 2, 5, None, 10, FAKE, FAKE, 10, None) == eb.ERR_NULL
     assert lib.elpa_trans_ev_band_to_full(4, 3, 2, None, 4, None, None, 4, None) == eb.OK          # K = 0
+
+
+# ------------------------------------------------------------------ FP32 variant (NEXT-3)
+def _call_f32(n, nbw, nev, hv, ht, q, ldq, opts=None):
+    op = ctypes.byref(eb.Opts(**opts)) if opts is not None else None
+    return eb._lib.elpa_trans_ev_tridi_to_band_f32(n, nbw, nev, hv, ht, q, ldq, None, op)
+
+
+def test_f32_validation_order_before_device():
+    assert _call_f32(-1, 4, 1, FAKE, FAKE, FAKE, 12) == eb.ERR_ARG
+    assert _call_f32(10, 0, 1, FAKE, FAKE, FAKE, 12) == eb.ERR_ARG
+    assert _call_f32(10, 4, 11, FAKE, FAKE, FAKE, 12) == eb.ERR_ARG
+    assert _call_f32(10, 4, 5, FAKE, FAKE, FAKE, 9) == eb.ERR_ARG          # ldq < n
+    assert _call_f32(10, 4, 5, None, FAKE, FAKE, 12) == eb.ERR_NULL
+    assert _call_f32(10, 4, 5, FAKE, FAKE, None, 12) == eb.ERR_NULL
+    assert _call_f32(10, 4, 5, FAKE, FAKE, FAKE, 10) == eb.ERR_ALIGN       # ldq % 4 != 0
+    assert _call_f32(10, 4, 5, FAKE, FAKE, ctypes.c_void_p(0x10008), 12) == eb.ERR_ALIGN
+    assert _call_f32(10, 8, 5, FAKE, FAKE, FAKE, 12, dict(kernel=eb.KERNEL_DMMA)) == eb.ERR_ARG
+    assert _call_f32(10, 6, 5, FAKE, FAKE, FAKE, 12, dict(kernel=eb.KERNEL_FFMA2)) == eb.ERR_ARG
+    assert _call_f32(10, 8, 5, FAKE, FAKE, FAKE, 12, dict(kernel=eb.KERNEL_FFMA2, depth_warps=3, col_warps=1,
+                                                         tiles_per_warp=1)) == eb.ERR_ARG
+    assert _call_f32(10, 8, 5, FAKE, FAKE, FAKE, 12, dict(groups_per_step=2)) == eb.ERR_ARG
+    assert _call_f32(2, 4, 2, None, None, None, 2) == eb.OK                # R == 0: nothing touched
+    assert _call_f32(50, 8, 0, None, None, None, 50) == eb.OK
+
+
+def test_f32_describe():
+    k, desc = eb.describe_f32(20000, 64, 20000)
+    assert k == 2 and "kernel=ffma2" in desc and "b8=8" in desc
+    k, desc = eb.describe_f32(100, 6, 10)
+    assert k == 1 and "kernel=reference_f32" in desc
+    # workspace: groups x (8 reflectors x (4*b8+2) pairs x 2 + 8 taus) floats
+    n, b = 4096, 32
+    b8 = b // 8
+    M = (n - 3) // b + 1
+    G0 = ((n - 2) >> 3) + 1
+    groups = sum(G0 - m * b8 for m in range(M))
+    assert f"ws={groups * (16 * (4 * b8 + 2) + 8) * 4}" in eb.describe_f32(n, b, 100)[1]
+    for nbw in (8, 16, 24, 64, 72, 128):
+        assert eb.describe_f32(1000, nbw, 100)[0] == 2

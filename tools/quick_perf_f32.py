@@ -1,0 +1,38 @@
+"""Timing sweep of the FP32 variant's shapes (NEXT-3; development tool, not the bench).
+Times the whole FP32 call (prep + apply) with CUDA events; FLOP credit as for FP64."""
+import json, os, sys
+import torch
+sys.path.insert(0, '.')
+import paper_1811_01277_b200 as eb
+from inputs import synthetic_reflectors_torch, synthetic_q_torch
+
+SHAPES = [tuple(int(v) for v in t.split(',')) for t in os.environ['SHAPES'].split()] if os.environ.get('SHAPES') else \
+    [(1, 2, 1), (2, 2, 1), (1, 4, 1), (2, 1, 1), (4, 2, 1), (1, 1, 2), (1, 2, 2), (2, 1, 2)]
+REPS = int(os.environ.get('REPS', '2'))
+cfgs = [(20000, 64, 20000), (20000, 64, 2000), (4096, 32, 4096)]
+if len(sys.argv) > 1:
+    cfgs = [tuple(int(v) for v in a.split(',')) for a in sys.argv[1:]]
+for (n, nbw, nev) in cfgs:
+    R = eb.hh_count(n, nbw)
+    dv, dt = synthetic_reflectors_torch(R, nbw, 1, device='cuda')
+    dv, dt = dv.float(), dt.float()
+    dq = synthetic_q_torch(n, 0, nev, 2, device='cuda').float()
+    fl = eb.credited_flops(n, nbw, nev)
+    for sh in [None] + SHAPES:
+        opts = None if sh is None else dict(kernel=eb.KERNEL_FFMA2, depth_warps=sh[0], col_warps=sh[1],
+                                            tiles_per_warp=sh[2])
+        try:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            eb.trans_ev_tridi_to_band(n, nbw, dv, dt, dq, opts=opts); torch.cuda.synchronize()
+            best = 1e30
+            for _ in range(REPS):
+                e0.record(); eb.trans_ev_tridi_to_band(n, nbw, dv, dt, dq, opts=opts); e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            print(json.dumps(dict(dtype="f32", n=n, nbw=nbw, nev=nev, shape=sh, ms=round(best, 3),
+                                  tflops=round(fl / best / 1e9, 3), desc=eb.describe_f32(n, nbw, nev, opts)[1])),
+                  flush=True)
+        except Exception as ex:
+            print(json.dumps(dict(n=n, nbw=nbw, nev=nev, shape=sh, error=str(ex))), flush=True)
+    del dv, dt, dq
+    torch.cuda.empty_cache()
