@@ -15,37 +15,41 @@ using namespace elpa_b200_host;
 
 namespace {
 
-// (D depth warps, CW column warps, NC 32-column blocks per warp) menus.  Full menu for
-// nbw = 8/16/32/64, a small one for the other multiples of 8 up to 128 (compile-time budget).
-#define ELPA_F32_SHAPES(X) X(1, 2, 1) X(2, 2, 1) X(1, 4, 1) X(2, 1, 1) X(4, 2, 1) X(1, 1, 2) X(1, 2, 2) X(2, 1, 2)
-#define ELPA_F32_SMALL_SHAPES(X) X(1, 2, 1) X(2, 2, 1)
-struct F32Shape { int D, CW, NC; };
-#define ELPA_F32_ENTRY(D_, CW_, NC_) {D_, CW_, NC_},
+// (D depth warps, CW column warps, NC 32-column blocks per warp, K groups per step) menus.
+// Full menu for nbw = 8/16/32/64, a small one for the other multiples of 8 up to 128
+// (compile-time budget).
+#define ELPA_F32_SHAPES(X) X(1, 2, 1, 1) X(2, 2, 1, 1) X(1, 4, 1, 1) X(2, 1, 1, 1) X(4, 2, 1, 1) X(1, 1, 2, 1) \
+    X(1, 2, 2, 1) X(2, 1, 2, 1) X(1, 1, 1, 1) X(1, 2, 1, 2) X(2, 2, 1, 2) X(2, 1, 1, 2)
+#define ELPA_F32_SMALL_SHAPES(X) X(1, 2, 1, 1) X(2, 2, 1, 1)
+struct F32Shape { int D, CW, NC, K; };
+#define ELPA_F32_ENTRY(D_, CW_, NC_, K_) {D_, CW_, NC_, K_},
 constexpr F32Shape kF32Shapes[] = {ELPA_F32_SHAPES(ELPA_F32_ENTRY)};
 constexpr F32Shape kF32SmallShapes[] = {ELPA_F32_SMALL_SHAPES(ELPA_F32_ENTRY)};
 
 bool f32_full_menu(int b8) { return b8 == 1 || b8 == 2 || b8 == 4 || b8 == 8; }
 bool f32_b8_supported(int64_t nbw) { return nbw % 8 == 0 && nbw >= 8 && nbw <= 128; }
 
-bool f32_shape_compiled(int b8, int D, int CW, int NC) {
+bool f32_shape_compiled(int b8, int D, int CW, int NC, int K) {
     if (f32_full_menu(b8)) {
         for (const F32Shape &s : kF32Shapes)
-            if (s.D == D && s.CW == CW && s.NC == NC) return true;
+            if (s.D == D && s.CW == CW && s.NC == NC && s.K == K) return true;
         return false;
     }
     for (const F32Shape &s : kF32SmallShapes)
-        if (s.D == D && s.CW == CW && s.NC == NC) return true;
+        if (s.D == D && s.CW == CW && s.NC == NC && s.K == K) return true;
     return false;
 }
 
-size_t f32_smem(int b8, int D, int CW, int NC) {
-    return size_t(3) * D * f32_blob_floats(b8) * 4 + size_t(2) * D * CW * NC * 2 * 32 * 16 +
-           size_t(2) * CW * NC * 2 * 32 * 16 + 64;
+size_t f32_smem(int b8, int D, int CW, int NC, int K) {
+    const size_t blob = size_t(f32_blob_floats(b8)) * 4;
+    const int stages = (K * D * blob * 3 <= 100 * 1024) ? 3 : 2;
+    return size_t(stages) * K * D * blob + size_t(2) * D * K * CW * NC * 2 * 32 * 16 +
+           size_t(2) * K * CW * NC * 2 * 32 * 16 + 64;
 }
 
 struct F32Plan {
     int kernel = ELPA_B200_KERNEL_REFERENCE;
-    int b8 = 0, D = 1, CW = 1, NC = 1;
+    int b8 = 0, D = 1, CW = 1, NC = 1, K = 1;
     int grid_req = 0;
     int64_t items = 0, nx = 0, grid = 1;
     int threads = 128;
@@ -60,7 +64,6 @@ int f32_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, 
     if (kernel == ELPA_B200_KERNEL_AUTO)
         kernel = f32_b8_supported(nbw) ? ELPA_B200_KERNEL_FFMA2 : ELPA_B200_KERNEL_REFERENCE;
     if (kernel == ELPA_B200_KERNEL_FFMA2 && !f32_b8_supported(nbw)) return ELPA_B200_ERR_ARG;
-    if (o && o->groups_per_step > 1) return ELPA_B200_ERR_ARG;      // one group per step
     p.kernel = kernel;
     if (kernel == ELPA_B200_KERNEL_REFERENCE) {
         p.threads = 128;
@@ -69,9 +72,11 @@ int f32_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, 
     }
     p.b8 = int(nbw / 8);
     int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NC = o ? o->tiles_per_warp : 0;
-    if (D == 0 && CW == 0 && NC == 0) { D = 1; CW = 2; NC = 1; }
-    if (!f32_shape_compiled(p.b8, D, CW, NC)) return ELPA_B200_ERR_ARG;
-    p.D = D; p.CW = CW; p.NC = NC;
+    int K = o ? o->groups_per_step : 0;
+    if (D == 0 && CW == 0 && NC == 0) { D = 2; CW = 2; NC = 1; }
+    if (K == 0) K = 1;
+    if (!f32_shape_compiled(p.b8, D, CW, NC, K)) return ELPA_B200_ERR_ARG;
+    p.D = D; p.CW = CW; p.NC = NC; p.K = K;
     p.grid_req = o ? o->grid_ctas : 0;
     if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
     const int64_t M = num_depths(n, nbw);
@@ -80,7 +85,7 @@ int f32_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, 
     p.items = p.nx * ((M + D - 1) / D);
     p.grid = p.items;
     p.threads = 32 * D * CW;
-    p.smem = f32_smem(p.b8, D, CW, NC);
+    p.smem = f32_smem(p.b8, D, CW, NC, K);
     if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * f32_blob_floats(p.b8) * 4 : 0;
     return ELPA_B200_OK;
@@ -104,11 +109,11 @@ int f32_launch_prep(int64_t n, const float *hh_v, const float *hh_tau, float *ws
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
 }
 
-template <int B8, int D, int CW, int NC>
+template <int B8, int D, int CW, int NC, int K>
 int f32_launch_shape(const F32Plan &p, int64_t n, int64_t nev, const float *ws, float *Q, int64_t ldq,
                      cudaStream_t s) {
-    using Cfg = F32Cfg<B8, D, CW, NC>;
-    auto kern = apply_f32_kernel<B8, D, CW, NC>;
+    using Cfg = F32Cfg<B8, D, CW, NC, K>;
+    auto kern = apply_f32_kernel<B8, D, CW, NC, K>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)) != cudaSuccess)
         return fail_cuda();
     int per_sm = 0;
@@ -133,8 +138,9 @@ int f32_launch_shape(const F32Plan &p, int64_t n, int64_t nev, const float *ws, 
 
 template <int B8>
 int f32_launch_b8(const F32Plan &p, int64_t n, int64_t nev, const float *ws, float *Q, int64_t ldq, cudaStream_t s) {
-#define ELPA_F32_CASE(D_, CW_, NC_) \
-    if (p.D == D_ && p.CW == CW_ && p.NC == NC_) return f32_launch_shape<B8, D_, CW_, NC_>(p, n, nev, ws, Q, ldq, s);
+#define ELPA_F32_CASE(D_, CW_, NC_, K_)                               \
+    if (p.D == D_ && p.CW == CW_ && p.NC == NC_ && p.K == K_) \
+        return f32_launch_shape<B8, D_, CW_, NC_, K_>(p, n, nev, ws, Q, ldq, s);
     if constexpr (B8 == 1 || B8 == 2 || B8 == 4 || B8 == 8) {
         ELPA_F32_SHAPES(ELPA_F32_CASE)
     } else {
@@ -191,8 +197,8 @@ int elpa_b200_describe_f32(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_
     int rc = f32_make_plan(n, nbw, nev, opts, p);
     if (rc != ELPA_B200_OK) return rc;
     if (buf && buflen)
-        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NC=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
-                 p.kernel == ELPA_B200_KERNEL_FFMA2 ? "ffma2" : "reference_f32", p.b8, p.D, p.CW, p.NC,
+        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NC=%d K=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
+                 p.kernel == ELPA_B200_KERNEL_FFMA2 ? "ffma2" : "reference_f32", p.b8, p.D, p.CW, p.NC, p.K,
                  (long long)p.items, p.grid_req, p.threads, p.smem, (long long)p.ws_bytes);
     if (hh_total(n, nbw) == 0 || nev == 0) return 0;
     return p.kernel == ELPA_B200_KERNEL_REFERENCE ? 1 : 2;

@@ -134,7 +134,7 @@ def test_f32_validation_order_before_device():
     assert _call_f32(10, 6, 5, FAKE, FAKE, FAKE, 12, dict(kernel=eb.KERNEL_FFMA2)) == eb.ERR_ARG
     assert _call_f32(10, 8, 5, FAKE, FAKE, FAKE, 12, dict(kernel=eb.KERNEL_FFMA2, depth_warps=3, col_warps=1,
                                                          tiles_per_warp=1)) == eb.ERR_ARG
-    assert _call_f32(10, 8, 5, FAKE, FAKE, FAKE, 12, dict(groups_per_step=2)) == eb.ERR_ARG
+    assert _call_f32(10, 8, 5, FAKE, FAKE, FAKE, 12, dict(groups_per_step=3)) == eb.ERR_ARG
     assert _call_f32(2, 4, 2, None, None, None, 2) == eb.OK                # R == 0: nothing touched
     assert _call_f32(50, 8, 0, None, None, None, 50) == eb.OK
 

@@ -55,32 +55,33 @@ def run32(eb, n, nbw, hv, tau, Q, opts=None):
     return dq.cpu().numpy()
 
 
-SHAPES = [(1, 2, 1), (2, 2, 1), (1, 4, 1), (2, 1, 1), (4, 2, 1), (1, 1, 2), (1, 2, 2), (2, 1, 2)]
+SHAPES = [(1, 2, 1, 1), (2, 2, 1, 1), (1, 4, 1, 1), (2, 1, 1, 1), (4, 2, 1, 1), (1, 1, 2, 1), (1, 2, 2, 1),
+          (2, 1, 2, 1), (1, 1, 1, 1), (1, 2, 1, 2), (2, 2, 1, 2), (2, 1, 1, 2)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("nbw", [8, 16, 32, 64])
 def test_f32_all_shapes(eb, shape, nbw):
-    D, CW, NC = shape
+    D, CW, NC, K = shape
     n, nev = 301, 45                          # ragged: n odd, nev not a multiple of 32
     hv, tau, Q, want = f32_case(n, nbw, nev, nbw * 11 + D, ldq=304)
     tol = bound(n, nbw)
     for grid in (0, 1, 2, 3):
         got = run32(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_FFMA2, depth_warps=D, col_warps=CW,
-                                                       tiles_per_warp=NC, grid_ctas=grid))
+                                                       tiles_per_warp=NC, grid_ctas=grid, groups_per_step=K))
         assert colerr(got[:, :n], want[:, :n]) <= tol, (shape, grid)
         assert np.array_equal(got[:, n:], Q[:, n:])      # ldq padding untouched
 
 
-@pytest.mark.parametrize("shape,grid", [((1, 2, 1), 0), ((1, 2, 1), 5), ((2, 2, 1), 0), ((4, 2, 1), 7),
-                                        ((1, 2, 2), 0), ((2, 1, 2), 3)])
+@pytest.mark.parametrize("shape,grid", [((1, 2, 1, 1), 0), ((1, 2, 1, 1), 5), ((2, 2, 1, 1), 0), ((4, 2, 1, 1), 7),
+                                        ((1, 2, 2, 1), 0), ((2, 1, 2, 1), 3), ((2, 2, 1, 2), 0), ((2, 1, 1, 2), 5)])
 def test_f32_multi_item_at_scale(eb, shape, grid):
     """many items per CTA, passes of one column block pipelining across CTAs"""
-    D, CW, NC = shape
+    D, CW, NC, K = shape
     n, nbw, nev = 2000, 64, 700
     hv, tau, Q, want = f32_case(n, nbw, nev, 41 + D * CW + NC)
     got = run32(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_FFMA2, depth_warps=D, col_warps=CW,
-                                                   tiles_per_warp=NC, grid_ctas=grid))
+                                                   tiles_per_warp=NC, grid_ctas=grid, groups_per_step=K))
     assert colerr(got, want) <= bound(n, nbw)
 
 
@@ -88,7 +89,7 @@ def test_f32_multi_item_at_scale(eb, shape, grid):
 def test_f32_nbw_range(eb, nbw):
     n, nev = 400, 70
     hv, tau, Q, want = f32_case(n, nbw, nev, 3 * nbw)
-    for opts in (None, dict(kernel=eb.KERNEL_FFMA2, depth_warps=2, col_warps=2, tiles_per_warp=1)):
+    for opts in (None, dict(kernel=eb.KERNEL_FFMA2, depth_warps=1, col_warps=2, tiles_per_warp=1)):
         got = run32(eb, n, nbw, hv, tau, Q, opts=opts)
         assert colerr(got[:, :n], want[:, :n]) <= bound(n, nbw), opts
 
@@ -131,7 +132,8 @@ def test_f32_guard_bands(eb):
     big[G:G + nev * ldq] = torch.from_numpy(Q.reshape(-1)).cuda()
     dq = big[G:G + nev * ldq].view(nev, ldq)
     for opts in (None, dict(kernel=eb.KERNEL_FFMA2, depth_warps=4, col_warps=2, tiles_per_warp=1),
-                 dict(kernel=eb.KERNEL_FFMA2, depth_warps=1, col_warps=2, tiles_per_warp=2)):
+                 dict(kernel=eb.KERNEL_FFMA2, depth_warps=1, col_warps=2, tiles_per_warp=2),
+                 dict(kernel=eb.KERNEL_FFMA2, depth_warps=2, col_warps=2, tiles_per_warp=1, groups_per_step=2)):
         dq.copy_(torch.from_numpy(Q).cuda())
         eb.trans_ev_tridi_to_band(n, nbw, torch.from_numpy(hv).cuda(), torch.from_numpy(tau).cuda(), dq, opts=opts)
         torch.cuda.synchronize()

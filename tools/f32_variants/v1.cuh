@@ -19,7 +19,7 @@
 // pair p0(a) = (7-a)/2 of the window, VP = 4*b8 + 2 pairs each (zeros outside [7-a, 7-a+L)),
 // then tau[8].
 #pragma once
-#include "kernel_dmma.cuh"
+#include "../../paper_1811_01277_b200/csrc/kernel_dmma.cuh"
 
 namespace elpa_b200 {
 
@@ -60,34 +60,33 @@ struct F32Group {
     static constexpr int VP = f32_vp(B8);
     static constexpr int NPAIR = 4 * B8 + 1;     // pairs a reflector spans (b rows, start parity)
     static constexpr int BLOB = int(f32_blob_floats(B8));
-    // applies the group to window pairs [OFF, OFF + NPW) of a register window of NW pairs
-    template <int OFF, int NW>
-    __device__ __forceinline__ static void apply(f2_t (&q)[NC][NW], const float *blob) {
+    __device__ __forceinline__ static void apply(f2_t (&q)[NC][NPW], const float *blob) {
         const ulonglong2 *vb = reinterpret_cast<const ulonglong2 *>(blob);
         const float *tau = blob + 16 * VP;
 #pragma unroll
         for (int a = 0; a < 8; a++) {
-            const int p0 = OFF + ((7 - a) >> 1);
+            const int p0 = (7 - a) >> 1;
             const ulonglong2 *v = vb + a * (VP / 2);
             // w = tau * v^T q: two accumulators per column (even / odd pair index)
-            f2_t acc[NC][2];
+            f2_t acc[NC][4];
 #pragma unroll
-            for (int t = 0; t < NC; t++) acc[t][0] = acc[t][1] = 0ull;
+            for (int t = 0; t < NC; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0ull;
 #pragma unroll
             for (int k2 = 0; k2 < VP / 2; k2++) {
                 const ulonglong2 vv = v[k2];
                 F32_VBARRIER();
 #pragma unroll
                 for (int t = 0; t < NC; t++) {
-                    acc[t][0] = ffma2(q[t][p0 + 2 * k2], vv.x, acc[t][0]);
-                    if (2 * k2 + 1 < NPAIR) acc[t][1] = ffma2(q[t][p0 + 2 * k2 + 1], vv.y, acc[t][1]);
+                    acc[t][2 * (k2 & 1)] = ffma2(q[t][p0 + 2 * k2], vv.x, acc[t][2 * (k2 & 1)]);
+                    if (2 * k2 + 1 < NPAIR)
+                        acc[t][2 * (k2 & 1) + 1] = ffma2(q[t][p0 + 2 * k2 + 1], vv.y, acc[t][2 * (k2 & 1) + 1]);
                 }
             }
             const float ta = tau[a];
             f2_t w2[NC];
 #pragma unroll
             for (int t = 0; t < NC; t++) {
-                const f2_t s2 = fadd2(acc[t][0], acc[t][1]);
+                const f2_t s2 = fadd2(fadd2(acc[t][0], acc[t][1]), fadd2(acc[t][2], acc[t][3]));
                 w2[t] = f2_splat(-ta * (f2_lo(s2) + f2_hi(s2)));
             }
             // q -= w v (v is re-read from shared memory: keeping the b floats of v live from the
@@ -181,70 +180,48 @@ __device__ __forceinline__ void f32_store_chunk(float *colp, bool ok, int n, int
         if (r + i < n) colp[r + i] = (i & 1) ? f2_hi(src[i >> 1]) : f2_lo(src[i >> 1]);
 }
 
-// compile-time loop: f(integral_constant<int, I>) for I = I0 .. I1-1
-template <int I0, int I1, class F>
-__device__ __forceinline__ void static_for(F &&f) {
-    if constexpr (I0 < I1) {
-        f(std::integral_constant<int, I0>{});
-        static_for<I0 + 1, I1>(f);
-    }
-}
-
-template <int B8, int D, int CW, int NC, int K>
+template <int B8, int D, int CW, int NC>
 struct F32Cfg {
     static constexpr int LAM = B8 + 1;
     using Group = F32Group<B8, NC>;
     static constexpr int BLOB = Group::BLOB;                // floats per prepared group
-    static constexpr int W = LAM + K - 1;                  // register window in chunks
-    static constexpr int NWP = 4 * W;                      // ... in row pairs
     static constexpr int NWARP = D * CW;
     static constexpr int THREADS = 32 * NWARP;
     static constexpr int COLS = CW * NC * 32;              // columns per work item
-    static constexpr int STAGES = (K * D * BLOB * 4 * 3 <= 100 * 1024) ? 3 : 2;
-    // shared memory: STAGES x K x D blobs, hand-off chunks [2][D][K][CW][NC][2][32] x 16 B,
-    // warp-0 intake chunks [2][K][CW][NC][2][32] x 16 B, barriers + the dequeued item index
-    static constexpr size_t SMEM_BLOBS = size_t(STAGES) * K * D * BLOB * sizeof(float);
-    static constexpr size_t SMEM_HAND = size_t(2) * D * K * CW * NC * 2 * 32 * 16;
-    static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NC * 2 * 32 * 16;
+    static constexpr int STAGES = 3;
+    // shared memory: STAGES x D blobs, hand-off chunks [2][D][CW][NC][2][32] x 16 B, warp-0
+    // intake chunks [2][CW][NC][2][32] x 16 B, barriers + the dequeued item index
+    static constexpr size_t SMEM_BLOBS = size_t(STAGES) * D * BLOB * sizeof(float);
+    static constexpr size_t SMEM_HAND = size_t(2) * D * CW * NC * 2 * 32 * 16;
+    static constexpr size_t SMEM_INTAKE = size_t(2) * CW * NC * 2 * 32 * 16;
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
-    // Register cap (__maxnreg__): the window is 8*W*NC floats.  NC = 1, K = 1 at nbw <= 64
-    // compiles without spills in 168 (6 CTAs of 64 threads per SM); larger windows get 255.
-    // (A minBlocks launch bound instead spills at the same count.)
-    static constexpr int REGCAP = (NC == 1 && K == 1 && B8 <= 8) ? 168 : 255;
+    // Register cap (__maxnreg__): the window is 8*LAM*NC floats.  NC = 1 at nbw <= 64 compiles
+    // without spills in 168 (6 CTAs of 64 threads per SM); NC = 2 or nbw > 64 get the full 255
+    // (nbw >= 112 with NC = 1 still spills a little).  A minBlocks launch bound instead spills
+    // at the same count.
+    static constexpr int REGCAP = (NC == 1 && B8 <= 8) ? 168 : 255;
 };
 
-// The persistent item kernel of kernel_dmma.cuh (work items, dynamic dequeue, progress words:
-// DESIGN.md §5) with FP32 windows, F32Group arithmetic and K groups per step.
-//
-// Step st of an item applies group-times tau = st*K + j, j = 0..K-1: depth warp d applies
-// group g = G - 1 - tau + d*K of depth m0 + d.  Its register window holds W = lambda + K - 1
-// chunks, top chunk T_d(st) = C0 - st*K - (K-1) + d*W, so group j sits at chunk offset
-// K-1-j and the K groups of a step need no data movement between them.  The D windows are
-// stacked without gaps and without chunks in transit: at the end of a step every warp emits
-// its bottom K chunks (to HBM from the deepest warp, else to warp d+1 through shared memory);
-// at the start of the next step it shifts its window down by K chunks and takes in K new top
-// chunks (HBM for warp 0, prefetched with cp.async one step ahead).  Depth m0+d+1 thus trails
-// depth m0+d by K groups, one step: the schedule legality of DESIGN.md §5 (a reflector of
-// depth m+1 overlaps only reflectors of depth m with a larger sweep index, all in groups
-// with index >= its own) holds with one barrier per step.  Register moves: 4*(W-K) pairs per
-// step, i.e. 4*(lambda-1)/K per group.
-template <int B8, int D, int CW, int NC, int K>
-__global__ void __maxnreg__((F32Cfg<B8, D, CW, NC, K>::REGCAP))
+// The persistent item kernel of kernel_dmma.cuh with one group per step (K = 1), FP32
+// windows and F32Group arithmetic.  Work item k = (pass p = k / NX, column block x = k % NX);
+// progress words and their protocol are identical (kernel_dmma.cuh).
+template <int B8, int D, int CW, int NC>
+__global__ void __maxnreg__((F32Cfg<B8, D, CW, NC>::REGCAP))
 apply_f32_kernel(int64_t n64, int64_t nev64, const float *__restrict__ blobs, float *Q, int64_t ldq,
                  uint64_t *prog, int pub_period) {
-    using Cfg = F32Cfg<B8, D, CW, NC, K>;
+    using Cfg = F32Cfg<B8, D, CW, NC>;
     using Group = typename Cfg::Group;
-    constexpr int W = Cfg::W;
-    constexpr int NWP = Cfg::NWP;
+    constexpr int LAM = Cfg::LAM;
+    constexpr int NPW = Group::NPW;
     constexpr int BLOB = Cfg::BLOB;
     constexpr int S = Cfg::STAGES;
     constexpr int COLS = Cfg::COLS;
     constexpr int B = 8 * B8;
-    constexpr int LAG = K;                                 // groups depth m+1 trails depth m
-    constexpr int SPAN = W;                                // chunk distance between stacked windows
+    constexpr int LAG = 2;                                 // groups depth m+1 trails depth m
+    constexpr int SPAN = LAM + 1;                          // chunk distance between stacked windows
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *sblob = reinterpret_cast<float *>(smem_raw);                                              // [S][K][D][BLOB]
+    float *sblob = reinterpret_cast<float *>(smem_raw);                                              // [S][D][BLOB]
     ulonglong2 *shand = reinterpret_cast<ulonglong2 *>(smem_raw + Cfg::SMEM_BLOBS);
     ulonglong2 *sintake = reinterpret_cast<ulonglong2 *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND + Cfg::SMEM_INTAKE);
@@ -257,15 +234,10 @@ apply_f32_kernel(int64_t n64, int64_t nev64, const float *__restrict__ blobs, fl
     const int C0 = (n - 2) >> 3;
     const int NX = (nev + COLS - 1) / COLS;
     const int NP = (M + D - 1) / D;
-    // hand-off slot (parity, receiving depth, chunk j of the step, column t, half h) / intake slot
-    auto hslot = [&](int par, int dd, int j, int t, int h) {
-        return (((((par * D + dd) * K + j) * CW + cw) * NC + t) * 2 + h) * 32 + lane;
+    auto hslot = [&](int par, int dd, int t, int h) {
+        return ((((par * D + dd) * CW + cw) * NC + t) * 2 + h) * 32 + lane;
     };
-    auto islot = [&](int par, int j, int t, int h) {
-        return ((((par * K + j) * CW + cw) * NC + t) * 2 + h) * 32 + lane;
-    };
-    // the blob ring is fed by one thread of the deepest depth row (no intake work there)
-    const bool issuer = threadIdx.x == 32 * (D - 1) * CW;
+    auto islot = [&](int par, int t, int h) { return (((par * CW + cw) * NC + t) * 2 + h) * 32 + lane; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; i++) mbar_init(&bars[i], 1);
@@ -294,39 +266,34 @@ apply_f32_kernel(int64_t n64, int64_t nev64, const float *__restrict__ blobs, fl
         }
         const int G = int(groups_at_depth(n64, B8, m0));
         const int dmax = min(D, M - m0) - 1;
-        const int NT = G + dmax * LAG;                     // group-times of this item
-        const int nsteps = (NT + K - 1) / K;
-        const int T0 = C0 - (K - 1) + d * SPAN;            // this warp's window top at step 0
+        const int NT = G + dmax * LAG;                     // steps (= group-times) of this item
 
-        // deepest warps' lowest emitted chunk after step st; chunks >= it are final
-        auto deep_cbot = [&](int st) { return C0 - st * K - (K - 1) + (D - 1) * SPAN + W - K; };
-        int pub_count = 0;
+        auto deep_cbot = [&](int st) { return C0 - st + (D - 1) * SPAN + LAM - 1; };
         auto pub_step = [&](int st) {
             const int cbot = deep_cbot(st);
-            return (pub_count == pub_period - 1 || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
+            const bool every = (st % pub_period) == pub_period - 1;
+            return (every || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
         };
         auto group_valid = [&](int tau, int dd) {
             const int g = G - 1 - tau + dd * LAG;
             return dd <= dmax && tau < NT && g >= 0 && g < G - dd * B8;
         };
-        auto issue = [&](int st) {                         // K x D blobs of step st -> ring stage
+        auto issue = [&](int st) {
             const int stg = (stage0 + st) % S;
             uint64_t *bar = &bars[stg];
             uint32_t bytes = 0;
-            for (int j = 0; j < K; j++)
-                for (int dd = 0; dd <= dmax; dd++)
-                    if (group_valid(st * K + j, dd)) bytes += BLOB * 4;
+            for (int dd = 0; dd <= dmax; dd++)
+                if (group_valid(st, dd)) bytes += BLOB * 4;
             mbar_arrive_expect_tx(bar, bytes);
-            for (int j = 0; j < K; j++)
-                for (int dd = 0; dd <= dmax; dd++)
-                    if (group_valid(st * K + j, dd)) {
-                        const int g = G - 1 - (st * K + j) + dd * LAG;
-                        const float *src = blobs + (group_base(n64, B8, m0 + dd) + g) * BLOB;
-                        bulk_g2s(sblob + ((stg * K + j) * D + dd) * BLOB, src, BLOB * 4, bar);
-                    }
+            for (int dd = 0; dd <= dmax; dd++)
+                if (group_valid(st, dd)) {
+                    const int g = G - 1 - st + dd * LAG;
+                    const float *src = blobs + (group_base(n64, B8, m0 + dd) + g) * BLOB;
+                    bulk_g2s(sblob + (stg * D + dd) * BLOB, src, BLOB * 4, bar);
+                }
         };
-        if (issuer)
-            for (int st = 0; st < S - 1 && st < nsteps; st++) issue(st);
+        if (threadIdx.x == 0)
+            for (int st = 0; st < S - 1 && st < NT; st++) issue(st);
 
         uint32_t seen = 0;
         auto await_chunk = [&](int c) {
@@ -345,98 +312,87 @@ apply_f32_kernel(int64_t n64, int64_t nev64, const float *__restrict__ blobs, fl
             }
             seen = __shfl_sync(0xffffffffu, seen, 0);
         };
-        // warp-0 intake of the K top chunks of step st (chunks T_0(st) + j), one step ahead
-        auto intake = [&](int st) {
-            const int top = T0 - st * K;
-            await_chunk(top);
+        auto intake = [&](int st) {                        // chunk entering after step st
+            const int c = C0 - st - 1;
+            await_chunk(c);
 #pragma unroll
-            for (int j = 0; j < K; j++)
-#pragma unroll
-                for (int t = 0; t < NC; t++)
-                    f32_load_chunk_async(&sintake[islot(st & 1, j, t, 0)], &sintake[islot(st & 1, j, t, 1)], qcol[t],
-                                         (okmask >> t) & 1, n, top + j);
+            for (int t = 0; t < NC; t++)
+                f32_load_chunk_async(&sintake[islot(st & 1, t, 0)], &sintake[islot(st & 1, t, 1)], qcol[t],
+                                     (okmask >> t) & 1, n, c);
             cp_async_commit();
         };
 
-        f2_t q[NC][NWP];
-        if (d == 0) await_chunk(T0);
+        f2_t q[NC][NPW];
+        if (d == 0) await_chunk(C0);
 #pragma unroll
         for (int t = 0; t < NC; t++)
 #pragma unroll
-            for (int i = 0; i < W; i++)
-                f32_load_chunk(&q[t][4 * i], qcol[t], (okmask >> t) & 1, n, T0 + i);
-        if (d == 0 && nsteps > 1) intake(1);
+            for (int i = 0; i < LAM; i++)
+                f32_load_chunk(&q[t][4 * i], qcol[t], (okmask >> t) & 1, n, C0 + d * SPAN + i);
+        if (d == 0) intake(0);
 
         for (int st = 0;; st++) {
-            if (st > 0) {
-                // take in the K new top chunks: shift the window down by K chunks
-                if (d == 0) {
-                    if (st + 1 < nsteps) intake(st + 1);
-                    if (st + 1 < nsteps) cp_async_wait<1>(); else cp_async_wait<0>();
-                }
-#pragma unroll
-                for (int t = 0; t < NC; t++) {
-#pragma unroll
-                    for (int i = NWP - 1; i >= 4 * K; i--) q[t][i] = q[t][i - 4 * K];
-#pragma unroll
-                    for (int j = 0; j < K; j++) {
-                        const ulonglong2 lo2 = (d == 0) ? sintake[islot(st & 1, j, t, 0)]
-                                                        : shand[hslot((st - 1) & 1, d, j, t, 0)];
-                        const ulonglong2 hi2 = (d == 0) ? sintake[islot(st & 1, j, t, 1)]
-                                                        : shand[hslot((st - 1) & 1, d, j, t, 1)];
-                        q[t][4 * j] = lo2.x; q[t][4 * j + 1] = lo2.y; q[t][4 * j + 2] = hi2.x; q[t][4 * j + 3] = hi2.y;
-                    }
-                }
-            }
-            if (issuer && st + S - 1 < nsteps) issue(st + S - 1);
+            if (threadIdx.x == 0 && st + S - 1 < NT) issue(st + S - 1);
+            if (d == 0 && st + 1 < NT) intake(st + 1);
             const uint32_t stage = uint32_t((stage0 + st) % S);
             const uint32_t par = (phase_bits >> stage) & 1u;
             phase_bits ^= (1u << stage);
-            bool waited = false;
-            static_for<0, K>([&](auto jc) {
-                constexpr int j = decltype(jc)::value;
-                if (group_valid(st * K + j, d)) {
-                    if (!waited) { mbar_wait(&bars[stage], par); waited = true; }
-                    Group::template apply<4 * (K - 1 - j), NWP>(q, sblob + ((stage * K + j) * D + d) * BLOB);
-                }
-            });
-            if (st + 1 >= nsteps) break;                   // final windows written back below
-            // emit the bottom K chunks (window chunks W-K .. W-1 = T_d + W - K + jj)
-            const int cb = T0 - st * K + W - K;
+            if (group_valid(st, d)) {
+                mbar_wait(&bars[stage], par);
+                Group::apply(q, sblob + (stage * D + d) * BLOB);
+            }
+            if (st + 1 >= NT) break;                       // final windows written back below
+            const int cbot = C0 - st + d * SPAN + LAM - 1;
             if (d == D - 1) {
 #pragma unroll
-                for (int jj = 0; jj < K; jj++)
-#pragma unroll
-                    for (int t = 0; t < NC; t++)
-                        f32_store_chunk(qcol[t], (okmask >> t) & 1, n, cb + jj, &q[t][4 * (W - K + jj)]);
+                for (int t = 0; t < NC; t++) f32_store_chunk(qcol[t], (okmask >> t) & 1, n, cbot, &q[t][NPW - 4]);
                 if (pub_step(st)) __threadfence();
             } else {
 #pragma unroll
-                for (int jj = 0; jj < K; jj++)
+                for (int t = 0; t < NC; t++) {
+                    shand[hslot(st & 1, d + 1, t, 0)] = make_ulonglong2(q[t][NPW - 4], q[t][NPW - 3]);
+                    shand[hslot(st & 1, d + 1, t, 1)] = make_ulonglong2(q[t][NPW - 2], q[t][NPW - 1]);
+                }
+            }
+            if (d == 0) cp_async_wait<1>();
 #pragma unroll
-                    for (int t = 0; t < NC; t++) {
-                        shand[hslot(st & 1, d + 1, jj, t, 0)] =
-                            make_ulonglong2(q[t][4 * (W - K + jj)], q[t][4 * (W - K + jj) + 1]);
-                        shand[hslot(st & 1, d + 1, jj, t, 1)] =
-                            make_ulonglong2(q[t][4 * (W - K + jj) + 2], q[t][4 * (W - K + jj) + 3]);
-                    }
+            for (int t = 0; t < NC; t++) {
+#pragma unroll
+                for (int i = NPW - 1; i >= 4; i--) q[t][i] = q[t][i - 4];
+                ulonglong2 lo2 = make_ulonglong2(0ull, 0ull), hi2 = make_ulonglong2(0ull, 0ull);
+                if (d == 0) {
+                    lo2 = sintake[islot(st & 1, t, 0)];
+                    hi2 = sintake[islot(st & 1, t, 1)];
+                } else if (st > 0) {                       // st == 0: rows below the matrix
+                    lo2 = shand[hslot((st + 1) & 1, d, t, 0)];
+                    hi2 = shand[hslot((st + 1) & 1, d, t, 1)];
+                }
+                q[t][0] = lo2.x; q[t][1] = lo2.y; q[t][2] = hi2.x; q[t][3] = hi2.y;
             }
             __syncthreads();
             if (threadIdx.x == 0 && pub_step(st)) st_release_u64(prog + k, uint64_t(C0 + 2 - deep_cbot(st)));
-            pub_count = (pub_count == pub_period - 1) ? 0 : pub_count + 1;
         }
         if (d == 0) cp_async_wait<0>();
-        // write back the final windows (no chunks are in transit between windows)
-        const int tf = T0 - (nsteps - 1) * K;
+        __syncthreads();
 #pragma unroll
         for (int t = 0; t < NC; t++)
 #pragma unroll
-            for (int i = 0; i < W; i++)
-                f32_store_chunk(qcol[t], (okmask >> t) & 1, n, tf + i, &q[t][4 * i]);
+            for (int i = 0; i < LAM; i++)
+                f32_store_chunk(qcol[t], (okmask >> t) & 1, n, C0 - (NT - 1) + d * SPAN + i, &q[t][4 * i]);
+        // the chunk in transit (emitted by warp d-1 in the last step, not yet taken) is final
+        if (d >= 1 && NT >= 2) {
+            const int c = C0 - (NT - 2) + (d - 1) * SPAN + LAM - 1;
+#pragma unroll
+            for (int t = 0; t < NC; t++) {
+                const ulonglong2 lo2 = shand[hslot(NT & 1, d, t, 0)], hi2 = shand[hslot(NT & 1, d, t, 1)];
+                const f2_t tmp[4] = {lo2.x, lo2.y, hi2.x, hi2.y};
+                f32_store_chunk(qcol[t], (okmask >> t) & 1, n, c, tmp);
+            }
+        }
         __threadfence();
-        __syncthreads();  // item complete: publish, and the smem ring/hand-off are free again
+        __syncthreads();
         if (threadIdx.x == 0) st_release_u64(prog + k, kPassDone);
-        stage0 = (stage0 + nsteps) % S;
+        stage0 = (stage0 + NT) % S;
     }
 }
 

@@ -7,7 +7,8 @@ import paper_1811_01277_b200 as eb
 from inputs import synthetic_reflectors_torch, synthetic_q_torch
 
 SHAPES = [tuple(int(v) for v in t.split(',')) for t in os.environ['SHAPES'].split()] if os.environ.get('SHAPES') else \
-    [(1, 2, 1), (2, 2, 1), (1, 4, 1), (2, 1, 1), (4, 2, 1), (1, 1, 2), (1, 2, 2), (2, 1, 2)]
+    [(1, 2, 1, 1), (2, 2, 1, 1), (1, 4, 1, 1), (2, 1, 1, 1), (4, 2, 1, 1), (1, 1, 2, 1), (1, 2, 2, 1), (2, 1, 2, 1),
+     (1, 1, 1, 1), (1, 2, 1, 2), (2, 2, 1, 2), (2, 1, 1, 2)]
 REPS = int(os.environ.get('REPS', '2'))
 cfgs = [(20000, 64, 20000), (20000, 64, 2000), (4096, 32, 4096)]
 if len(sys.argv) > 1:
@@ -20,7 +21,7 @@ for (n, nbw, nev) in cfgs:
     fl = eb.credited_flops(n, nbw, nev)
     for sh in [None] + SHAPES:
         opts = None if sh is None else dict(kernel=eb.KERNEL_FFMA2, depth_warps=sh[0], col_warps=sh[1],
-                                            tiles_per_warp=sh[2])
+                                            tiles_per_warp=sh[2], groups_per_step=sh[3])
         try:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             eb.trans_ev_tridi_to_band(n, nbw, dv, dt, dq, opts=opts); torch.cuda.synchronize()
