@@ -332,6 +332,8 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         return ((((par * D + dd) * K + j) * CW + cw) * NCT + t) * 32 + lane;
     };
     auto islot = [&](int par, int j, int t) { return (((par * K + j) * CW + cw) * NCT + t) * 32 + lane; };
+    // the fragment ring is fed by one thread of the deepest depth row, which has no HBM intake
+    const bool issuer = threadIdx.x == 32 * (D - 1) * CW;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; i++) mbar_init(&bars[i], 1);
@@ -369,10 +371,10 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         // publish steps: every pub_period steps (host-chosen) and the step whose emission
         // finalises chunk C0 (a next pass waiting for its first window starts at once); only
         // while the deepest warps' emissions are real chunks
+        int pub_count = 0;                                 // == st % pub_period
         auto pub_step = [&](int st) {
             const int cbot = C0 - (st * K + K - 1) + (D - 1) * SPAN + LAM - 1;
-            const bool every = (st % pub_period) == pub_period - 1;
-            return (every || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
+            return (pub_count == pub_period - 1 || cbot == C0) && cbot <= C0 + 1 && cbot >= 0;
         };
         auto group_valid = [&](int tau, int dd) {
             const int g = G - 1 - tau + dd * LAG;
@@ -394,7 +396,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                         bulk_g2s(sblob + ((stg * K + j) * D + dd) * BLOB, src, BLOB * 8, bar);
                     }
         };
-        if (threadIdx.x == 0)
+        if (issuer)
             for (int st = 0; st < S - 1 && st < nsteps; st++) issue(st);
 
         // cross-pass dependency (warp 0 only): chunk c must be final from pass p-1
@@ -440,7 +442,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
 
         bool done = false;
         for (int st = 0; !done; st++) {
-            if (threadIdx.x == 0 && st + S - 1 < nsteps) issue(st + S - 1);
+            if (issuer && st + S - 1 < nsteps) issue(st + S - 1);
             if (d == 0 && st + 1 < nsteps) intake(st + 1);
             const uint32_t stage = uint32_t((stage0 + st) % S);
             const uint32_t par = (phase_bits >> stage) & 1u;
@@ -490,6 +492,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 const int cbot = C0 - (st * K + K - 1) + (D - 1) * SPAN + LAM - 1;
                 st_release_u64(prog + k, uint64_t(C0 + 2 - cbot));
             }
+            pub_count = (pub_count == pub_period - 1) ? 0 : pub_count + 1;
         }
         if (d == 0) cp_async_wait<0>();   // drain any unused intake before slot reuse
         __syncthreads();                  // the last step's hand-off writes are visible below
