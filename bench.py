@@ -31,6 +31,7 @@ METRIC = "trans_ev_tridi_to_band FP64 TFLOP/s (2*n^2*nev) and % roofline, 1/2/4/
 UNIT = "TFLOP/s"
 CFG_INDEX = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
 PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.jsonl")
+PEAKS32_FILE = os.path.join(ROOT, "profiles", "fp32_peaks_r01.jsonl")
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
 
 
@@ -43,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="f32: the NEXT-3 single-precision variant (not the BASELINE metric)")
     return ap.parse_args()
 
 
@@ -149,10 +152,127 @@ def reference_arm(args):
     return 0
 
 
+def run_f32(args):
+    """--dtype f32: the FP32 variant on the same workload, inputs rounded
+    to FP32 once.  One step = [N>1: NCCL broadcast of the FP32 reflectors] + one call of
+    elpa_trans_ev_tridi_to_band_f32 (prep + apply kernels).  Not the BASELINE metric: a
+    separate line with metric "... FP32 ..."."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1811_01277_b200 as eb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, nbw, nev = CONFIGS[args.config]
+    seed = config_seed(CFG_INDEX[args.config])
+    R = eb.hh_count(n, nbw)
+    c0, c1 = (rank * nev) // world, ((rank + 1) * nev) // world
+    nev_loc = c1 - c0
+    stream = torch.cuda.current_stream(dev)
+    hh = torch.empty(R * (nbw + 1), dtype=torch.float32, device=dev)
+    if rank == 0:
+        hv_d, tau_d = synthetic_reflectors_torch(R, nbw, seed, device=dev)
+        hh[:R * nbw].copy_(hv_d.reshape(-1))
+        hh[R * nbw:].copy_(tau_d)
+        del hv_d, tau_d
+    hh_v, hh_tau = hh[:R * nbw].view(R, nbw), hh[R * nbw:]
+    ldq = (n + 3) // 4 * 4
+    Q = torch.zeros((nev_loc, ldq), dtype=torch.float32, device=dev)
+    Q[:, :n] = synthetic_q_torch(n, c0, c1, seed, device=dev).float()
+    Q0 = Q.clone()
+    nlaunch, desc = eb.describe_f32(n, nbw, nev_loc)
+    torch.cuda.synchronize()
+
+    def step():
+        if world > 1:
+            dist.broadcast(hh, src=0)
+        eb.trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Q, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    flops_total = 4.0 * nbw * nev * R
+    value = flops_total / (ms_per_step * 1e-3) / 1e12
+
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        # the oracle (fp64) recomputes 2 columns of a fresh single call from the same FP32 inputs
+        import oracle
+        cols = [0, nev_loc - 1]
+        Qt = Q0[cols].clone()
+        eb.trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Qt, stream=stream)
+        torch.cuda.synchronize()
+        s_arr, L_arr = oracle.schedule(n, nbw)
+        want = Q0[cols].double().cpu().numpy()
+        step_r = 1 << 22
+        for r1 in range(R, 0, -step_r):
+            r0 = max(0, r1 - step_r)
+            want = oracle.apply(hh_v[r0:r1].double().cpu().numpy(), hh_tau[r0:r1].double().cpu().numpy(),
+                                s_arr[r0:r1], L_arr[r0:r1], want)
+        got = Qt.double().cpu().numpy()
+        parity = float((np.linalg.norm(got[:, :n] - want[:, :n], axis=1) /
+                        np.linalg.norm(want[:, :n], axis=1)).max())
+
+    peak = None
+    try:
+        for line in open(PEAKS32_FILE):
+            r = json.loads(line)
+            if r.get("test") == "ffma2_f32x2":
+                peak = max(peak or 0, r["tflops"])
+    except OSError:
+        pass
+    peak = peak or 71.46
+    achieved = 4.0 * nbw * nev_loc * R / (ms_per_step * 1e-3) / 1e12
+    if rank == 0:
+        print(json.dumps({
+            "metric": "trans_ev_tridi_to_band FP32 TFLOP/s (NEXT-3 variant; credited 4*nbw*nev per reflector)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (FP64 recipe rounded to FP32)",
+            "config": {"workload": f"{args.config} n={n} nbw={nbw} nev={nev}", "n": n, "nbw": nbw, "nev": nev,
+                       "nev_per_gpu": nev_loc, "reflectors": R, "parallelism": f"nev-sharded x{world}",
+                       "l2": "inputs larger than L2 (Q shard %.2f GB, hh_v %.2f GB)" % (nev_loc * n * 4 / 1e9, R * nbw * 4 / 1e9),
+                       "kernel": desc, "step": ("bcast+" if world > 1 else "") + "prep+apply (one f32 call)"},
+            "clocks": clk.summary(), "gpu_launches": nlaunch * args.steps,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "apply_f32_kernel (+ prep_f32_kernel: whole call timed)",
+                         "peak_source": "measured packed FP32 FMA (fma.rn.f32x2) peak on this pool's B200 (profiles/fp32_peaks_r01.jsonl)"},
+            "parity_colwise_rel_err_sampled": parity}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.dtype == "f32":
+        return run_f32(args)
 
     import numpy as np
     import torch
