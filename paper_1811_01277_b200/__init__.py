@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libelpa_b200.so")
+# ELPA_B200_LIB: development override (A/B timing of library builds); default: the in-tree build
+_SO = os.environ.get("ELPA_B200_LIB") or os.path.join(_HERE, "libelpa_b200.so")
 
 OK, ERR_ARG, ERR_NULL, ERR_ALIGN, ERR_DEVICE, ERR_CUDA, ERR_SPACE = 0, -1, -2, -3, -4, -5, -6
 KERNEL_AUTO, KERNEL_REFERENCE, KERNEL_DMMA, KERNEL_DFMA, KERNEL_FFMA2 = 0, 1, 2, 3, 4

@@ -332,8 +332,9 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         return ((((par * D + dd) * K + j) * CW + cw) * NCT + t) * 32 + lane;
     };
     auto islot = [&](int par, int j, int t) { return (((par * K + j) * CW + cw) * NCT + t) * 32 + lane; };
-    // the fragment ring is fed by one thread of the deepest depth row, which has no HBM intake
-    const bool issuer = threadIdx.x == 32 * (D - 1) * CW;
+    // the fragment ring is fed by the last warp (deepest depth row: no HBM intake when D > 1;
+    // with D = 1 it spares warp 0, which also dequeues items and publishes progress)
+    const bool issuer = threadIdx.x == 32 * (D * CW - 1);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; i++) mbar_init(&bars[i], 1);
