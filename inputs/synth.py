@@ -155,3 +155,46 @@ def synthetic_q_torch(n, c0, c1, seed, ldq=None, device="cpu", chunk_cols=1024):
         cnt = torch.arange(a * n, b * n, dtype=torch.int64, device=device)
         out[a - c0:b - c0, :n] = uniform_pm1_torch(seed ^ TAG_Q, cnt).reshape(b - a, n)
     return out
+
+
+# ---- generalized EVP inputs (NEXT-4) -----------------------------------------------------
+TAG_SPD = 0x6A5B4C3D2E1F0918
+TAG_TRIL = 0x19283746AFBECDD0
+
+
+def spd_matrix(n, seed):
+    """Random symmetric positive definite B = C C^T / n + I, C uniform [-1,1) (row-major
+    stream), so cond(B) = O(1) and its Cholesky factor is well conditioned."""
+    n = int(n)
+    C = uniform_pm1_np(seed ^ TAG_SPD, np.arange(n * n, dtype=np.uint64)).reshape(n, n)
+    return C @ C.T / max(n, 1) + np.eye(n)
+
+
+def lower_triangular_cm_np(n, c0, c1, seed, ldl=None):
+    """Columns [c0, c1) of a well-conditioned random lower-triangular n x n matrix, as the
+    (c1-c0, ldl) row-major view of its column-major storage: L[i][c] = 1.5 + u/2 on the
+    diagonal, u/n below it, 0 above (u uniform [-1,1) from element counter c*n + i), so
+    L = D (I + N) with ||N||_2 < 1/2."""
+    ldl = n if ldl is None else ldl
+    out = np.zeros((c1 - c0, ldl), dtype=np.float64)
+    if c1 > c0 and n > 0:
+        u = uniform_pm1_np(seed ^ TAG_TRIL, np.arange(c0 * n, c1 * n, dtype=np.uint64)).reshape(c1 - c0, n)
+        rows = np.arange(n)[None, :]
+        cols = np.arange(c0, c1)[:, None]
+        out[:, :n] = np.where(rows > cols, u / n, np.where(rows == cols, 1.5 + 0.5 * u, 0.0))
+    return out
+
+
+def lower_triangular_cm_torch(n, c0, c1, seed, ldl=None, device="cpu", chunk_cols=1024):
+    """torch version of lower_triangular_cm_np (bitwise identical), generated on `device`."""
+    import torch
+    ldl = n if ldl is None else ldl
+    out = torch.zeros((c1 - c0, ldl), dtype=torch.float64, device=device)
+    rows = torch.arange(n, device=device)[None, :]
+    for a in range(c0, c1, chunk_cols):
+        b = min(c1, a + chunk_cols)
+        u = uniform_pm1_torch(seed ^ TAG_TRIL, torch.arange(a * n, b * n, dtype=torch.int64, device=device)).reshape(b - a, n)
+        cols = torch.arange(a, b, device=device)[:, None]
+        out[a - c0:b - c0, :n] = torch.where(rows > cols, u / n, torch.where(rows == cols, 1.5 + 0.5 * u,
+                                                                              torch.zeros_like(u)))
+    return out

@@ -11,6 +11,7 @@ What it computes (PAPER.md = /root/reference/PAPER.md):
     library dense/tridiagonal eigensolver, lowest nev pairs ascending (R7).
   * apply: Q_out = H_0 H_1 ... H_{R-1} Q, one reflector at a time in exact reverse
     generation order (Eq. 6) — oracle.c:oracle_apply.
+  * gen_back: V = L^-T Vtilde for the generalized EVP (Eq. 7; NEXT-4).
 Pins (tests/test_oracle_*.py) tie every function to mathematics other than itself:
 explicit reflector products, LAPACK dsytrd/dormqr at nbw = n-1, similarity, residual,
 closed-form Toeplitz spectra, SPEC worked examples (tests/golden/).
@@ -54,6 +55,8 @@ def _load():
         lib.oracle_reduce_to_band.argtypes = [i64, i64, p, p, p, p]
         lib.oracle_apply_full.restype = None
         lib.oracle_apply_full.argtypes = [i64, i64, p, i64, p, p, p, i64, i64, ctypes.c_int]
+        lib.oracle_gen_back.restype = None
+        lib.oracle_gen_back.argtypes = [i64, i64, p, i64, p, i64, ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -219,3 +222,42 @@ def make_case_full(n, nbw, nev, seed):
     Qfull = apply_full(V1, tau1, s1, Qband, n)
     return dict(A=A, band=band, V1=V1, tau1=tau1, s1=s1, hh_v=hh_v, hh_tau=hh_tau, s2=s2, L2=L2, d=d, e=e,
                 lam=lam, Qin=Qin, Qband=Qband, Qfull=Qfull)
+
+
+# ------------------------------------------------------------------ generalized EVP (NEXT-4)
+def gen_back(L, Q, nthreads=None):
+    """V = (L^{-1})^T Vtilde (Eq. 7) by backward substitution per column
+    (oracle.c:oracle_gen_back).  L: (n, n) lower-triangular numpy matrix (mathematical layout);
+    Q: (nev, ldq) row-major view of the column-major n x nev block.  Returns a new array."""
+    lib = _load()
+    L = np.asarray(L, dtype=np.float64)
+    n = L.shape[0]
+    Lcm = np.ascontiguousarray(L.T)                  # row i = column i of L (column-major storage)
+    Q = np.array(Q, dtype=np.float64, order="C", copy=True)
+    nev, ldq = Q.shape
+    if n and nev:
+        lib.oracle_gen_back(n, nev, _ptr(Lcm), n, _ptr(Q), ldq, int(nthreads or os.cpu_count() or 1))
+    return Q
+
+
+def make_case_generalized(n, nbw, nev, seed):
+    """The generalized EVP A V = B V Lambda through the whole two-stage pipeline:
+    B = L L^T (Cholesky, library), Atilde = L^-1 A L^-T (library triangular solves), the
+    two-stage solve of make_case_full on Atilde, then V = L^-T Vtilde (gen_back)."""
+    from inputs import dense_symmetric, spd_matrix
+    from scipy.linalg import solve_triangular
+    A = dense_symmetric(n, seed)
+    B = spd_matrix(n, seed)
+    L = np.linalg.cholesky(B)
+    X = solve_triangular(L, A, lower=True)
+    At = solve_triangular(L, X.T, lower=True).T
+    At = 0.5 * (At + At.T)
+    band, V1, tau1, s1, _ = reduce_to_band(At, nbw)
+    hh_v, hh_tau, s2, L2, d, e = chase(band)
+    lam, Vhat = tridiag_eig(d, e, nev)
+    Qin = np.ascontiguousarray(Vhat.T)
+    Qband = apply(hh_v, hh_tau, s2, L2, Qin)
+    Qt = apply_full(V1, tau1, s1, Qband, n)
+    V = gen_back(L, Qt)
+    return dict(A=A, B=B, L=L, At=At, lam=lam, Qt=Qt, V=V, band=band, hh_v=hh_v, hh_tau=hh_tau, s2=s2, L2=L2,
+                V1=V1, tau1=tau1, s1=s1, Qin=Qin, Qband=Qband)

@@ -284,3 +284,22 @@ void oracle_apply_full(int64_t n, int64_t K, const double *V, int64_t ldv, const
         }
     }
 }
+
+/* NEXT-4: generalized back-transformation V = (L^{-1})^H Vtilde (Eq. 7;
+ * B = L L^H is the Cholesky factorisation of P:99-101; real case: L^{-T}).  Per column, plain
+ * backward substitution with U = L^T:  for i = n-1 .. 0:
+ *     v_i = (q_i - sum_{k = i+1}^{n-1} L[k][i] v_k) / L[i][i]      (k increasing)
+ * L: n x n lower triangular, column-major with leading dimension ldl (column i contiguous);
+ * Q: nev x ldq (row c = column c), overwritten with V. */
+void oracle_gen_back(int64_t n, int64_t nev, const double *L, int64_t ldl, double *Q, int64_t ldq, int nthreads) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t c = 0; c < nev; c++) {
+        double *q = Q + c * ldq;
+        for (int64_t i = n - 1; i >= 0; i--) {
+            const double *li = L + i * ldl;                 /* column i of L */
+            double sum = 0.0;
+            for (int64_t k = i + 1; k < n; k++) sum += li[k] * q[k];
+            q[i] = (q[i] - sum) / li[i];
+        }
+    }
+}

@@ -55,3 +55,11 @@ def test_synthetic_reflectors_torch_bitwise():
     assert np.array_equal(v, vt.numpy())
     # tau = 2/||v||^2: same value up to the summation order of the norm
     assert np.allclose(tau, taut.numpy(), rtol=1e-15, atol=0)
+
+
+def test_lower_triangular_torch_matches_numpy():
+    import torch
+    from inputs import lower_triangular_cm_np, lower_triangular_cm_torch
+    a = lower_triangular_cm_np(37, 3, 30, 77, ldl=40)
+    b = lower_triangular_cm_torch(37, 3, 30, 77, ldl=40, chunk_cols=5).numpy()
+    assert np.array_equal(a, b)
