@@ -194,6 +194,23 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
                                const double *hh1_tau, double *Q, int64_t ldq, elpa_b200_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * NEXT-4: generalized back-transformation.  For the generalized EVP A x = lambda B x with the
+ * Cholesky factorisation B = L L^H and the standard problem of
+ * Atilde = L^{-1} A L^{-H}, the last step of the solver maps its eigenvectors
+ * back:  V = (L^{-1})^H Vtilde  (Eq. 7; real case: L^{-T}).
+ * L : device, n x n lower triangular, column-major (ldl >= n); only the lower triangle
+ *     (diagonal included) is read; its diagonal must be nonzero (not checked).
+ * Q : device, n x nev column-major (ldq >= n): in Vtilde, out V (in place).
+ * Blocked left-looking triangular solve: 128 x 128 diagonal blocks inverted by an own kernel,
+ * the products are DGEMMs on the FP64 tensor cores (cuBLAS, loaded at run time:
+ * ELPA_B200_ERR_CUDA if it cannot be loaded).  Asynchronous on `stream`.
+ * Errors: ERR_ARG (n < 0, nev < 0, nev > n, ldl or ldq < max(1, n), sizes beyond 32-bit
+ * BLAS), ERR_NULL, ERR_DEVICE, ERR_CUDA; n == 0 or nev == 0 is OK without memory access.
+ * ------------------------------------------------------------------------------------- */
+int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int64_t ldl, double *Q, int64_t ldq,
+                                    elpa_b200_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * NEXT-3: FP32 variant.  ELPA offers the whole solver in single precision, and
  * single precision in the eigen-steps is where the paper's 1.3-1.5x SCF gains come from
  * (P:663-692).  Same operation, reflector order, storage conventions, validation order and

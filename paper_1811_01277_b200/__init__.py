@@ -32,6 +32,8 @@ def _load():
     for f in (lib.elpa_trans_ev_tridi_to_band_ex, lib.elpa_trans_ev_tridi_to_band_host):
         f.restype = i32
         f.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
+    lib.elpa_generalized_back_transform.restype = i32
+    lib.elpa_generalized_back_transform.argtypes = [i64, i64, p, i64, p, i64, p]
     lib.elpa_trans_ev_tridi_to_band_f32.restype = i32
     lib.elpa_trans_ev_tridi_to_band_f32.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
     lib.elpa_b200_describe_f32.restype = i32
@@ -199,6 +201,21 @@ def apply_prepared(n, nbw, workspace, Q, hh_v=None, hh_tau=None, stream=None, op
                                        _dev_ptr(hh_tau, "hh_tau"), wptr, nbytes, _dev_ptr(Q, "Q"),
                                        int(ldq), s, op)
     _check(rc, "elpa_b200_apply_prepared")
+    return Q
+
+
+def generalized_back_transform(n, L, Q, stream=None):
+    """V = L^{-T} Vtilde in place (elpa_generalized_back_transform, NEXT-4; Eq. 7).  L: float64
+    CUDA tensor (n, ldl) = row-major view of the column-major lower-triangular factor (row i =
+    column i of L); Q: (nev, ldq) as for trans_ev_tridi_to_band."""
+    nev, ldq = _q_ldq(Q)
+    if L.dim() != 2 or L.stride(1) != 1:
+        raise ValueError("L must be an (n, ldl) tensor with unit stride along ldl")
+    ldl = L.stride(0) if L.shape[0] > 1 else L.shape[1]
+    s = _stream_handle(stream, Q.device)
+    rc = _lib.elpa_generalized_back_transform(int(n), int(nev), _dev_ptr(L, "L"), int(ldl), _dev_ptr(Q, "Q"),
+                                              int(ldq), s)
+    _check(rc, "elpa_generalized_back_transform")
     return Q
 
 

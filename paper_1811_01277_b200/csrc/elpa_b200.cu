@@ -17,6 +17,7 @@
 #include "kernel_prep.cuh"
 #include "kernel_reference.cuh"
 #include "band_to_full.cuh"
+#include "gen_back.cuh"
 
 #include <dlfcn.h>
 
@@ -710,7 +711,23 @@ const Cublas &cublas() {
 }
 constexpr int kOpN = 0, kOpT = 1;
 constexpr int64_t kB2FPanel = 128;
+
+// One cuBLAS handle per host thread and device, created on first use (handle creation costs
+// milliseconds; the handle carries no problem state), bound to stream s.  nullptr on failure;
+// `dev` receives the current device (handles of devices >= 64 are not cached: destroy them).
+cublas_handle_t cublas_handle(cudaStream_t s, int &dev) {
+    const Cublas &cb = cublas();
+    thread_local cublas_handle_t handles[64] = {};
+    dev = 0;
+    cudaGetDevice(&dev);
+    cublas_handle_t h = (dev >= 0 && dev < 64) ? handles[dev] : nullptr;
+    if (!h && cb.create(&h) != 0) h = nullptr;
+    if (h && dev >= 0 && dev < 64) handles[dev] = h;
+    if (h && cb.set_stream(h, s) != 0) return nullptr;
+    return h;
+}
 }  // namespace
+
 
 extern "C" {
 
@@ -743,15 +760,9 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
     double *T = reinterpret_cast<double *>(buf + up(bV) + up(bG));
     double *W = reinterpret_cast<double *>(buf + up(bV) + 2 * up(bG)), *W2 = reinterpret_cast<double *>(
                                                                               buf + up(bV) + 2 * up(bG) + up(bW));
-    // one cuBLAS handle per host thread and device, created on first use (handle creation
-    // costs milliseconds; the handle carries no problem state, the stream is set per call)
-    thread_local cublas_handle_t handles[64] = {};
     int dev = 0;
-    cudaGetDevice(&dev);
-    cublas_handle_t h = (dev >= 0 && dev < 64) ? handles[dev] : nullptr;
-    if (!h && cb.create(&h) != 0) h = nullptr;
-    if (h && dev >= 0 && dev < 64) handles[dev] = h;
-    if (!h || cb.set_stream(h, s) != 0) rc = ELPA_B200_ERR_CUDA;
+    cublas_handle_t h = cublas_handle(s, dev);
+    if (!h) rc = ELPA_B200_ERR_CUDA;
     const double one = 1.0, zero = 0.0, mone = -1.0;
     if (rc == ELPA_B200_OK) {
         dim3 g(unsigned(std::min<int64_t>(1024, (n * P + 255) / 256)), unsigned(np));
@@ -777,6 +788,55 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
             cb.dgemm(h, kOpN, kOpN, int(P), int(nev), int(P), &one, T + p * P * P, int(P), W, int(P), &zero, W2,
                      int(P)) != 0 ||
             cb.dgemm(h, kOpN, kOpN, int(m), int(nev), int(P), &mone, vp, int(m), W2, int(P), &one, q, int(ldq)) != 0)
+            rc = ELPA_B200_ERR_CUDA;
+    }
+    if (h && !(dev >= 0 && dev < 64)) cb.destroy(h);
+    if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    if (rc != ELPA_B200_OK) cudaGetLastError();
+    return rc;
+}
+
+
+int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int64_t ldl, double *Q, int64_t ldq,
+                                    elpa_b200_stream_t stream) {
+    if (n < 0 || nev < 0 || nev > n || ldl < (n > 1 ? n : 1) || ldq < (n > 1 ? n : 1)) return ELPA_B200_ERR_ARG;
+    if (n == 0 || nev == 0) return ELPA_B200_OK;
+    if (!L || !Q) return ELPA_B200_ERR_NULL;
+    if (n > INT32_MAX || nev > INT32_MAX || ldq > INT32_MAX || ldl > INT32_MAX) return ELPA_B200_ERR_ARG;
+    int rc = check_device();
+    if (rc != ELPA_B200_OK) return rc;
+    const Cublas &cb = cublas();
+    if (!cb.ok) return ELPA_B200_ERR_CUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    constexpr int NB = kGbBlock;
+    const int64_t nb = (n + NB - 1) / NB;
+    const size_t bInv = size_t(nb) * NB * NB * 8, bT = size_t(NB) * nev * 8;
+    char *buf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), ((bInv + 255) & ~size_t(255)) + bT, s) != cudaSuccess)
+        return fail_cuda();
+    double *Linv = reinterpret_cast<double *>(buf), *T = reinterpret_cast<double *>(buf + ((bInv + 255) & ~size_t(255)));
+    int dev = 0;
+    cublas_handle_t h = cublas_handle(s, dev);
+    if (!h) rc = ELPA_B200_ERR_CUDA;
+    const size_t smem = size_t(NB) * NB * 8;
+    if (rc == ELPA_B200_OK &&
+        cudaFuncSetAttribute(gb_trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        rc = ELPA_B200_ERR_CUDA;
+    if (rc == ELPA_B200_OK) {
+        gb_trinv_kernel<<<unsigned(nb), NB, smem, s>>>(n, L, ldl, Linv);
+        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    }
+    const double one = 1.0, zero = 0.0, mone = -1.0;
+    for (int64_t b = nb - 1; rc == ELPA_B200_OK && b >= 0; b--) {
+        const int64_t r0 = b * NB, m = std::min<int64_t>(NB, n - r0), r1 = r0 + m;
+        if (r1 < n && cb.dgemm(h, kOpT, kOpN, int(m), int(nev), int(n - r1), &mone, L + r0 * ldl + r1, int(ldl),
+                               Q + r1, int(ldq), &one, Q + r0, int(ldq)) != 0)
+            rc = ELPA_B200_ERR_CUDA;
+        if (rc == ELPA_B200_OK &&
+            (cb.dgemm(h, kOpT, kOpN, int(m), int(nev), int(m), &one, Linv + b * NB * NB, NB, Q + r0, int(ldq), &zero, T,
+                      NB) != 0 ||
+             cudaMemcpy2DAsync(Q + r0, size_t(ldq) * 8, T, size_t(NB) * 8, size_t(m) * 8, size_t(nev),
+                               cudaMemcpyDeviceToDevice, s) != cudaSuccess))
             rc = ELPA_B200_ERR_CUDA;
     }
     if (h && !(dev >= 0 && dev < 64)) cb.destroy(h);

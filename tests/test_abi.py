@@ -153,3 +153,15 @@ def test_f32_describe():
     assert f"ws={groups * (16 * (4 * b8 + 2) + 8) * 4}" in eb.describe_f32(n, b, 100)[1]
     for nbw in (8, 16, 24, 64, 72, 128):
         assert eb.describe_f32(1000, nbw, 100)[0] == 2
+
+
+def test_generalized_back_transform_validation():
+    f = eb._lib.elpa_generalized_back_transform
+    assert f(-1, 1, FAKE, 10, FAKE, 10, None) == eb.ERR_ARG
+    assert f(10, 11, FAKE, 10, FAKE, 10, None) == eb.ERR_ARG       # nev > n
+    assert f(10, 5, FAKE, 9, FAKE, 10, None) == eb.ERR_ARG         # ldl < n
+    assert f(10, 5, FAKE, 10, FAKE, 9, None) == eb.ERR_ARG         # ldq < n
+    assert f(10, 5, None, 10, FAKE, 10, None) == eb.ERR_NULL
+    assert f(10, 5, FAKE, 10, None, 10, None) == eb.ERR_NULL
+    assert f(0, 0, None, 1, None, 1, None) == eb.OK                # nothing to do, nothing touched
+    assert f(10, 0, None, 10, None, 10, None) == eb.OK
