@@ -37,7 +37,8 @@ def run_gen(eb, n, Lcm, Q):
 def test_gen_back_vs_oracle(eb, n, nev):
     ldl, ldq = n + 3, n + 5
     Lcm = lower_triangular_cm_np(n, 0, n, 100 + n, ldl=ldl)
-    Lcm[:, :n] += np.triu(np.full((n, n), np.nan), 1)       # the strict upper triangle must never be read
+    # Lcm[c, r] = L[r][c]: its strict lower triangle is L's strict upper one, never to be read
+    Lcm[:, :n] += np.tril(np.full((n, n), np.nan), -1)
     Q = synthetic_q_np(n, 0, nev, 200 + n, ldq=ldq)
     Q[:, n:] = 7.0
     L = np.nan_to_num(Lcm[:, :n].T, nan=0.0)
