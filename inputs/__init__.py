@@ -10,4 +10,5 @@ from .synth import (  # noqa: F401
     GAMMA, splitmix64_np, uniform_pm1_np, uniform_pm1_torch,
     band_matrix, dense_symmetric, synthetic_reflectors, synthetic_reflectors_torch, synthetic_q_np, synthetic_q_torch,
     config_seed, CONFIGS, spd_matrix, lower_triangular_cm_np, lower_triangular_cm_torch,
+    band_matrix_c, synthetic_reflectors_c, synthetic_q_c_np,
 )

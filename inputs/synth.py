@@ -198,3 +198,47 @@ def lower_triangular_cm_torch(n, c0, c1, seed, ldl=None, device="cpu", chunk_col
         out[a - c0:b - c0, :n] = torch.where(rows > cols, u / n, torch.where(rows == cols, 1.5 + 0.5 * u,
                                                                               torch.zeros_like(u)))
     return out
+
+
+# ---- complex (NEXT-3, Hermitian) inputs ---------------------------------------------------
+TAG_BAND_C = 0x4E3D2C1B0A998877
+TAG_HHV_C = 0x7A6B5C4D3E2F1001
+TAG_TAU_C = 0x1122334455667788
+TAG_Q_C = 0x0F1E2D3C4B5A6978
+
+
+def band_matrix_c(n, nbw, seed):
+    """Random Hermitian band matrix in lower band storage ((nbw+1, n) complex, row d = d-th
+    sub-diagonal): real and imaginary parts uniform [-1,1) from element counters 2k, 2k+1 of
+    the flattened storage (k = d*n + c); the diagonal is real."""
+    n, nbw = int(n), int(nbw)
+    u = uniform_pm1_np(seed ^ TAG_BAND_C, np.arange(2 * (nbw + 1) * n, dtype=np.uint64)).reshape(nbw + 1, n, 2)
+    band = u[..., 0] + 1j * u[..., 1]
+    band[0] = band[0].real
+    for dd in range(1, nbw + 1):
+        band[dd, n - dd:] = 0.0
+    return band
+
+
+def synthetic_reflectors_c(R, nbw, seed):
+    """Complex synthetic reflectors: v_0 = 1, v_i (i >= 1) complex uniform [-1,1)^2,
+    tau = (1 + exp(i phi)) / ||v||^2 with phi uniform [-pi, pi) (then H = I - tau v v^H is
+    unitary).  Returns (hh_v (R, nbw) complex128, hh_tau (R,) complex128)."""
+    R, nbw = int(R), int(nbw)
+    u = uniform_pm1_np(seed ^ TAG_HHV_C, np.arange(2 * R * nbw, dtype=np.uint64)).reshape(R, nbw, 2)
+    v = u[..., 0] + 1j * u[..., 1]
+    v[:, 0] = 1.0
+    phi = np.pi * uniform_pm1_np(seed ^ TAG_TAU_C, np.arange(R, dtype=np.uint64))
+    tau = (1.0 + np.exp(1j * phi)) / np.sum(np.abs(v) ** 2, axis=1)
+    return v, tau
+
+
+def synthetic_q_c_np(n, c0, c1, seed, ldq=None):
+    """Columns [c0, c1) of a complex synthetic n x nev block: element (i, c) = u[2(c*n+i)] +
+    i u[2(c*n+i)+1].  Returns (c1-c0, ldq) complex128 (row c = column c)."""
+    ldq = n if ldq is None else ldq
+    out = np.zeros((c1 - c0, ldq), dtype=np.complex128)
+    if c1 > c0 and n > 0:
+        u = uniform_pm1_np(seed ^ TAG_Q_C, np.arange(2 * c0 * n, 2 * c1 * n, dtype=np.uint64)).reshape(c1 - c0, n, 2)
+        out[:, :n] = u[..., 0] + 1j * u[..., 1]
+    return out

@@ -12,6 +12,7 @@ What it computes (PAPER.md = /root/reference/PAPER.md):
   * apply: Q_out = H_0 H_1 ... H_{R-1} Q, one reflector at a time in exact reverse
     generation order (Eq. 6) — oracle.c:oracle_apply.
   * gen_back: V = L^-T Vtilde for the generalized EVP (Eq. 7; NEXT-4).
+  * chase_c / apply_c / make_case_c: the complex Hermitian case (NEXT-3, DESIGN R15).
 Pins (tests/test_oracle_*.py) tie every function to mathematics other than itself:
 explicit reflector products, LAPACK dsytrd/dormqr at nbw = n-1, similarity, residual,
 closed-form Toeplitz spectra, SPEC worked examples (tests/golden/).
@@ -55,6 +56,10 @@ def _load():
         lib.oracle_reduce_to_band.argtypes = [i64, i64, p, p, p, p]
         lib.oracle_apply_full.restype = None
         lib.oracle_apply_full.argtypes = [i64, i64, p, i64, p, p, p, i64, i64, ctypes.c_int]
+        lib.oracle_chase_c.restype = i64
+        lib.oracle_chase_c.argtypes = [i64, i64, p, p, p, p, p, p, p]
+        lib.oracle_apply_c.restype = None
+        lib.oracle_apply_c.argtypes = [i64, i64, i64, p, p, p, p, p, i64, ctypes.c_int]
         lib.oracle_gen_back.restype = None
         lib.oracle_gen_back.argtypes = [i64, i64, p, i64, p, i64, ctypes.c_int]
         _lib = lib
@@ -261,3 +266,89 @@ def make_case_generalized(n, nbw, nev, seed):
     V = gen_back(L, Qt)
     return dict(A=A, B=B, L=L, At=At, lam=lam, Qt=Qt, V=V, band=band, hh_v=hh_v, hh_tau=hh_tau, s2=s2, L2=L2,
                 V1=V1, tau1=tau1, s1=s1, Qin=Qin, Qband=Qband)
+
+
+# ------------------------------------------------------------------ complex Hermitian (NEXT-3)
+def chase_c(band):
+    """Hermitian band -> tridiagonal chase (oracle.c:oracle_chase_c, zlarfg convention).
+    band: (nbw+1, n) complex lower band storage.  Returns (hh_v (R, nbw) complex, hh_tau (R,)
+    complex, s, L, d (n,) real, e (n-1,) complex)."""
+    lib = _load()
+    band = np.ascontiguousarray(band, dtype=np.complex128)
+    nb1, n = band.shape
+    nbw = nb1 - 1
+    R = count(n, nbw)
+    hh_v = np.zeros((max(R, 1), max(nbw, 1)), dtype=np.complex128)
+    tau = np.zeros(max(R, 1), dtype=np.complex128)
+    s = np.zeros(max(R, 1), dtype=np.int64)
+    L = np.zeros(max(R, 1), dtype=np.int64)
+    d = np.zeros(max(n, 1), dtype=np.float64)
+    e = np.zeros(max(n - 1, 1), dtype=np.complex128)
+    r = lib.oracle_chase_c(n, nbw, _ptr(band), _ptr(hh_v), _ptr(tau), _ptr(s), _ptr(L), _ptr(d), _ptr(e))
+    if r != R:
+        raise RuntimeError(f"oracle_chase_c returned {r}, expected {R}")
+    return hh_v[:R, :nbw], tau[:R], s[:R], L[:R], d[:n], e[:max(n - 1, 0)]
+
+
+def apply_c(hh_v, hh_tau, s, L, Q, nthreads=None):
+    """Q (nev, ldq) complex; returns H_0 ... H_{R-1} Q (H_r = I - tau_r v_r v_r^H)."""
+    lib = _load()
+    Q = np.array(Q, dtype=np.complex128, order="C", copy=True)
+    nev, ldq = Q.shape
+    hh_v = np.ascontiguousarray(hh_v, dtype=np.complex128)
+    R, nbw = hh_v.shape if hh_v.ndim == 2 else (0, 1)
+    if R > 0 and nev > 0:
+        lib.oracle_apply_c(nbw, nev, R, _ptr(hh_v), _ptr(np.ascontiguousarray(hh_tau, dtype=np.complex128)),
+                           _ptr(np.ascontiguousarray(s, dtype=np.int64)), _ptr(np.ascontiguousarray(L, dtype=np.int64)),
+                           _ptr(Q), ldq, int(nthreads or os.cpu_count() or 1))
+    return Q
+
+
+def tridiag_eig_c(d, e, nev):
+    """Lowest nev eigenpairs of the Hermitian tridiagonal T (real d, complex e = T(i+1, i)).
+    T = D T_r D^H with the unitary diagonal D (D_0 = 1, D_{i+1} = D_i e_i / |e_i|, 1 where
+    e_i = 0) and the real symmetric tridiagonal T_r (d, |e|): eigenvectors D Vhat_r
+    (R15).  Returns (lam, Vhat (n, nev) complex)."""
+    n = len(d)
+    ph = np.ones(n, dtype=np.complex128)
+    ae = np.abs(e)
+    for i in range(n - 1):
+        ph[i + 1] = ph[i] * (e[i] / ae[i] if ae[i] != 0 else 1.0)
+    lam, Vr = tridiag_eig(np.asarray(d, dtype=np.float64), ae, nev)
+    return lam, ph[:, None] * Vr
+
+
+def dense_from_band_c(band):
+    nb1, n = band.shape
+    B = np.zeros((n, n), dtype=np.complex128)
+    for dd in range(nb1):
+        idx = np.arange(n - dd)
+        B[idx + dd, idx] = band[dd, :n - dd]
+        B[idx, idx + dd] = np.conj(band[dd, :n - dd])
+    return B
+
+
+def residual_c(band, Q, lam):
+    """||B X - X Lambda||_F / (n ||B||_F), X = Q[:, :n]^T (columns = eigenvectors), B Hermitian band."""
+    nb1, n = band.shape
+    X = np.asarray(Q)[:, :n].T
+    BX = band[0].real[:, None] * X
+    for dd in range(1, nb1):
+        bd = band[dd, :n - dd][:, None]
+        BX[dd:] += bd * X[:-dd]
+        BX[:-dd] += np.conj(bd) * X[dd:]
+    nrmB = np.sqrt(np.sum(band[0].real ** 2) + 2.0 * np.sum(np.abs(band[1:]) ** 2))
+    return float(np.linalg.norm(BX - X * lam[None, :]) / (n * nrmB))
+
+
+def make_case_c(n, nbw, nev, seed):
+    """Complex Hermitian case: band -> chase -> tridiagonal eig (with the phase scaling) ->
+    back-transformation.  Returns dict(band, hh_v, hh_tau, s, L, d, e, lam, Qin, Qref)."""
+    from inputs import band_matrix_c
+    band = band_matrix_c(n, nbw, seed)
+    hh_v, hh_tau, s, L, d, e = chase_c(band)
+    lam, Vhat = tridiag_eig_c(d, e, nev)
+    Qin = np.ascontiguousarray(Vhat.T)
+    Qref = apply_c(hh_v, hh_tau, s, L, Qin)
+    return dict(n=n, nbw=nbw, nev=nev, band=band, hh_v=hh_v, hh_tau=hh_tau, s=s, L=L, d=d, e=e, lam=lam,
+                Qin=Qin, Qref=Qref)

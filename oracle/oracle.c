@@ -303,3 +303,155 @@ void oracle_gen_back(int64_t n, int64_t nev, const double *L, int64_t ldl, doubl
         }
     }
 }
+
+/* ====================================================================================
+ * NEXT-3 (second half): the complex Hermitian case.  ELPA's complex solver
+ * chases a Hermitian band matrix with complex reflectors Q_i = I - beta_i v_i v_i^H
+ * (P:117-121 written for the complex case).  Same geometry as the real chase (R1,
+ * R2): reflector (j, m) on rows [s, s+L), s = j+1+m*b, L = min(b, n-s) >= 2.  Convention
+ * LAPACK zlarfg (R15): H^H (alpha; x) = (beta; 0) with beta REAL, H = I - tau v v^H,
+ * v_0 = 1, tau complex; the chase applies A <- H^H A H; the back-transformation is
+ *     Q_out = H_0 H_1 ... H_{R-1} Q,     per reflector  w = tau * sum_i conj(v_i) q_i,  q_i -= w v_i.
+ * Complex numbers are C99 `double complex`; products and sums are the plain formulas
+ * (a+bi)(c+di) = (ac-bd) + (ad+bc)i, -ffp-contract=off.
+ * ==================================================================================== */
+#include <complex.h>
+
+typedef struct { int64_t n, ld; double complex *w; } hermband;
+
+static double complex hb_get(const hermband *A, int64_t r, int64_t c) {
+    if (r < c) {
+        if (c - r >= A->ld) return 0.0;
+        return conj(A->w[r * A->ld + (c - r)]);
+    }
+    if (r - c >= A->ld) return 0.0;
+    return A->w[c * A->ld + (r - c)];
+}
+
+static int hb_set(hermband *A, int64_t r, int64_t c, double complex x) {
+    if (r < c) { int64_t t = r; r = c; c = t; x = conj(x); }
+    if (r - c >= A->ld) return x != 0.0;
+    A->w[c * A->ld + (r - c)] = x;
+    return 0;
+}
+
+/* zlarfg: alpha = x0, sigma^2 = sum_{i>=1} |x_i|^2.  sigma == 0 and Im(alpha) == 0 -> identity
+ * (tau = 0, beta = alpha).  Otherwise beta = -sign(Re alpha) sqrt(|alpha|^2 + sigma^2)
+ * (sign(0) = +1), tau = (beta - alpha) / beta, v_i = x_i / (alpha - beta). */
+static void plain_zlarfg(int64_t L, const double complex *x, double complex *v, double complex *tau, double *beta) {
+    double complex alpha = x[0];
+    double sig2 = 0.0;
+    for (int64_t i = 1; i < L; i++) sig2 += creal(x[i]) * creal(x[i]) + cimag(x[i]) * cimag(x[i]);
+    v[0] = 1.0;
+    if (sig2 == 0.0 && cimag(alpha) == 0.0) {
+        for (int64_t i = 1; i < L; i++) v[i] = 0.0;
+        *tau = 0.0;
+        *beta = creal(alpha);
+        return;
+    }
+    double nrm = sqrt(creal(alpha) * creal(alpha) + cimag(alpha) * cimag(alpha) + sig2);
+    double bt = (creal(alpha) >= 0.0) ? -nrm : nrm;
+    *tau = (bt - alpha) / bt;
+    double complex scal = alpha - bt;
+    for (int64_t i = 1; i < L; i++) v[i] = x[i] / scal;
+    *beta = bt;
+}
+
+/* Hermitian band -> real-diagonal tridiagonal chase recording every reflector.
+ *   band_in : (b+1) x n complex, band_in[dd*n + c] = B(c+dd, c) (the diagonal's imaginary part is ignored)
+ *   hh_v    : R x b complex (v_0 = 1, zero past L), hh_tau : R complex
+ *   d (n) real, e (n-1) complex: T(i+1, i) (real except possibly e[n-2], which no reflector touches)
+ * Returns R, or -1 if a nonzero value would leave the 3b storage. */
+int64_t oracle_chase_c(int64_t n, int64_t b, const double complex *band_in,
+                       double complex *hh_v, double complex *hh_tau, int64_t *s_out, int64_t *L_out,
+                       double *d, double complex *e) {
+    hermband A;
+    A.n = n;
+    A.ld = 3 * b + 1;
+    A.w = (double complex *)calloc((size_t)(n * A.ld), sizeof(double complex));
+    for (int64_t c = 0; c < n; c++)
+        for (int64_t dd = 0; dd <= b && c + dd < n; dd++)
+            A.w[c * A.ld + dd] = dd == 0 ? creal(band_in[c]) : band_in[dd * n + c];
+    int64_t wmax = 5 * b + 2;
+    double complex *win = (double complex *)malloc(sizeof(double complex) * (size_t)(wmax * wmax));
+    double complex *x = (double complex *)malloc(sizeof(double complex) * (size_t)(b + 1));
+    double complex *v = (double complex *)malloc(sizeof(double complex) * (size_t)(b + 1));
+    int64_t r = 0;
+    int bad = 0;
+    if (n >= 3 && b >= 2) {
+        for (int64_t j = 0; j <= n - 3; j++) {
+            int64_t col = j;
+            for (int64_t s = j + 1; s <= n - 2; s += b) {
+                int64_t L = (n - s < b) ? (n - s) : b;
+                for (int64_t i = 0; i < L; i++) x[i] = hb_get(&A, s + i, col);
+                double complex tau;
+                double beta;
+                plain_zlarfg(L, x, v, &tau, &beta);
+                if (tau != 0.0) {
+                    int64_t k0 = s - 2 * b; if (k0 < 0) k0 = 0;
+                    int64_t k1 = s + L + 2 * b; if (k1 > n) k1 = n;
+                    int64_t K = k1 - k0;
+                    int64_t o = s - k0;
+                    for (int64_t i = 0; i < L; i++)
+                        for (int64_t t = 0; t < K; t++) {
+                            win[(o + i) * K + t] = hb_get(&A, s + i, k0 + t);
+                            win[t * K + o + i] = hb_get(&A, k0 + t, s + i);
+                        }
+                    /* left: rows [o, o+L) <- H^H rows = rows - conj(tau) v (v^H rows) */
+                    for (int64_t cc = 0; cc < K; cc++) {
+                        double complex p = 0.0;
+                        for (int64_t i = 0; i < L; i++) p += conj(v[i]) * win[(o + i) * K + cc];
+                        p *= conj(tau);
+                        for (int64_t i = 0; i < L; i++) win[(o + i) * K + cc] -= p * v[i];
+                    }
+                    /* right: cols [o, o+L) <- cols H = cols - tau (cols v) v^H */
+                    for (int64_t rr = 0; rr < K; rr++) {
+                        double complex q = 0.0;
+                        for (int64_t i = 0; i < L; i++) q += win[rr * K + o + i] * v[i];
+                        q *= tau;
+                        for (int64_t i = 0; i < L; i++) win[rr * K + o + i] -= q * conj(v[i]);
+                    }
+                    for (int64_t i = 0; i < L; i++)
+                        for (int64_t t = 0; t < K; t++) {
+                            if (t <= o + i) bad |= hb_set(&A, s + i, k0 + t, win[(o + i) * K + t]);
+                            else            bad |= hb_set(&A, k0 + t, s + i, win[t * K + o + i]);
+                        }
+                    for (int64_t i = 0; i < L; i++)           /* Hermitian: real diagonal */
+                        A.w[(s + i) * A.ld] = creal(A.w[(s + i) * A.ld]);
+                }
+                bad |= hb_set(&A, s, col, beta);
+                for (int64_t i = 1; i < L; i++) bad |= hb_set(&A, s + i, col, 0.0);
+                for (int64_t i = 0; i < b; i++) hh_v[r * b + i] = (i < L) ? v[i] : 0.0;
+                hh_tau[r] = tau;
+                s_out[r] = s;
+                L_out[r] = L;
+                r++;
+                col = s;
+            }
+        }
+    }
+    for (int64_t i = 0; i < n; i++) d[i] = creal(hb_get(&A, i, i));
+    for (int64_t i = 0; i + 1 < n; i++) e[i] = hb_get(&A, i + 1, i);
+    free(win); free(x); free(v); free(A.w);
+    return bad ? -1 : r;
+}
+
+/* Complex back-transformation, one reflector at a time in exact reverse generation order:
+ * for r = R-1 .. 0, per column:  w = tau_r * sum_{i<L} conj(v_i) q[s+i]  (v_0 = 1, increasing i),
+ * q[s+i] -= w * v_i.  hh_v: R x nbw complex; Q: nev x ldq complex (row c = column c). */
+void oracle_apply_c(int64_t nbw, int64_t nev, int64_t R, const double complex *hh_v, const double complex *hh_tau,
+                    const int64_t *s_arr, const int64_t *L_arr, double complex *Q, int64_t ldq, int nthreads) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t c = 0; c < nev; c++) {
+        double complex *q = Q + c * ldq;
+        for (int64_t r = R - 1; r >= 0; r--) {
+            const double complex *v = hh_v + r * nbw;
+            int64_t s = s_arr[r], L = L_arr[r];
+            double complex sum = q[s];
+            for (int64_t i = 1; i < L; i++) sum += conj(v[i]) * q[s + i];
+            double complex w = hh_tau[r] * sum;
+            q[s] -= w;
+            for (int64_t i = 1; i < L; i++) q[s + i] -= w * v[i];
+        }
+    }
+}
