@@ -230,6 +230,27 @@ int elpa_trans_ev_tridi_to_band_f32(int64_t n, int64_t nbw, int64_t nev, const f
 int elpa_b200_describe_f32(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *opts,
                            char *buf, size_t buflen);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3 (second half): complex Hermitian variant.  ELPA's complex solver chases a
+ * Hermitian band matrix with complex reflectors H_r = I - tau_r v_r v_r^H (zlarfg
+ * convention, R15).  Same geometry, order and error codes as the real entry:
+ *      Q <- H_0 H_1 ... H_{R-1} Q,   per reflector  w = tau_r v_r^H q,  q -= w v_r.
+ * Complex data are interleaved (re, im) doubles (C99 double complex / cuDoubleComplex layout):
+ *   hh_v : device, nbw x R complex (column r = reflector r), element 0 treated as 1;
+ *   hh_tau: device, R complex;  Q: device, n x nev complex, ldq >= n (complex elements),
+ *   16-byte aligned (else ERR_ALIGN).
+ * opts (may be NULL): kernel AUTO (DMMA when nbw % 8 == 0 and nbw <= 128, else REFERENCE),
+ *   ELPA_B200_KERNEL_DMMA (complex compact-WY groups on FP64 tensor cores, 4 real DMMAs per
+ *   complex product) or ELPA_B200_KERNEL_REFERENCE (one thread per column, bitwise the CPU
+ *   oracle); depth_warps D, col_warps CW, tiles_per_warp = complex 8-column tiles per warp;
+ *   groups_per_step must be 0 or 1.  Asynchronous on `stream`.
+ * ------------------------------------------------------------------------------------- */
+int elpa_trans_ev_tridi_to_band_c64(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
+                                    double *Q, int64_t ldq, elpa_b200_stream_t stream, const elpa_b200_opts *opts);
+/* As elpa_b200_describe, for the complex entry point. */
+int elpa_b200_describe_c64(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *opts,
+                           char *buf, size_t buflen);
+
 /* Static description of an error code. */
 const char *elpa_b200_strerror(int code);
 

@@ -34,6 +34,10 @@ def _load():
         f.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
     lib.elpa_generalized_back_transform.restype = i32
     lib.elpa_generalized_back_transform.argtypes = [i64, i64, p, i64, p, i64, p]
+    lib.elpa_trans_ev_tridi_to_band_c64.restype = i32
+    lib.elpa_trans_ev_tridi_to_band_c64.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
+    lib.elpa_b200_describe_c64.restype = i32
+    lib.elpa_b200_describe_c64.argtypes = [i64, i64, i64, p, ctypes.c_char_p, sz]
     lib.elpa_trans_ev_tridi_to_band_f32.restype = i32
     lib.elpa_trans_ev_tridi_to_band_f32.argtypes = [i64, i64, i64, p, p, p, i64, p, p]
     lib.elpa_b200_describe_f32.restype = i32
@@ -138,11 +142,19 @@ def _q_ldq(Q):
 def trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Q, stream=None, opts=None):
     """Q <- H_0 H_1 ... H_{R-1} Q in place on the GPU (elpa_trans_ev_tridi_to_band[_ex]).
     Asynchronous on `stream` (default: torch's current stream).  float32 tensors go to the
-    FP32 variant (elpa_trans_ev_tridi_to_band_f32, NEXT-3); all three must share the dtype."""
+    FP32 variant (elpa_trans_ev_tridi_to_band_f32, NEXT-3), complex128 tensors to the complex
+    Hermitian variant (elpa_trans_ev_tridi_to_band_c64); all three must share the dtype."""
     import torch
     nev, ldq = _q_ldq(Q)
     o, op = _opts_ptr(opts)
     s = _stream_handle(stream, Q.device)
+    if isinstance(Q, torch.Tensor) and Q.dtype == torch.complex128:
+        z = torch.complex128
+        rc = _lib.elpa_trans_ev_tridi_to_band_c64(int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v", z),
+                                                  _dev_ptr(hh_tau, "hh_tau", z), _dev_ptr(Q, "Q", z), int(ldq), s,
+                                                  op)
+        _check(rc, "elpa_trans_ev_tridi_to_band_c64")
+        return Q
     if isinstance(Q, torch.Tensor) and Q.dtype == torch.float32:
         f = torch.float32
         rc = _lib.elpa_trans_ev_tridi_to_band_f32(int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v", f),
@@ -217,6 +229,16 @@ def generalized_back_transform(n, L, Q, stream=None):
                                               int(ldq), s)
     _check(rc, "elpa_generalized_back_transform")
     return Q
+
+
+def describe_c64(n, nbw, nev, opts=None):
+    """(launches, description) of the complex entry point's plan (elpa_b200_describe_c64)."""
+    o, op = _opts_ptr(opts)
+    buf = ctypes.create_string_buffer(512)
+    rc = _lib.elpa_b200_describe_c64(int(n), int(nbw), int(nev), op, buf, 512)
+    if rc < 0:
+        raise ElpaB200Error(rc, "elpa_b200_describe_c64")
+    return rc, buf.value.decode()
 
 
 def describe_f32(n, nbw, nev, opts=None):

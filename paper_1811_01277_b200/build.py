@@ -1,5 +1,5 @@
 """Build the C-ABI library libelpa_b200.so in-tree (sm_100a SASS only, static cudart).
-The translation units (FP64 path, FP32 path) compile in parallel, then link."""
+The translation units (FP64, FP32 and complex paths) compile in parallel, then link."""
 import os
 import subprocess
 import sys
@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libelpa_b200.so")
-SOURCES = [os.path.join(CSRC, "elpa_b200.cu"), os.path.join(CSRC, "elpa_b200_f32.cu")]
+SOURCES = [os.path.join(CSRC, "elpa_b200.cu"), os.path.join(CSRC, "elpa_b200_f32.cu"),
+           os.path.join(CSRC, "elpa_b200_c64.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
     [os.path.join(ROOT, "include", "elpa_b200.h")]
 

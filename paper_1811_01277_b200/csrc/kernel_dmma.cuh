@@ -117,7 +117,7 @@ __device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
 // q[t][i] in the m8n8k4 accumulator layout (lane l: rows 8i + 2(l%4) + {0,1} of column l/4).
 // Two policies compute the same compact-WY group, Q_W <- Q_W - V_g T^T V_g^T Q_W:
 // ---------------------------------------------------------------------------------------
-enum { KIND_DMMA = 0, KIND_DFMA = 1 };
+enum { KIND_DMMA = 0, KIND_DFMA = 1, KIND_ZMMA = 2 };
 
 // FP64 tensor cores: 2*LAM + 2*LAM DMMA.8x8x4 per tile, no shuffles.  Blob layout (prep
 // kernel): dot B-fragments of U = -V_g T [LAM][32 lanes][2], update B-fragments of V_g
@@ -254,8 +254,103 @@ struct DfmaGroup {
     }
 };
 
+// Complex Hermitian case (NEXT-3, R15) on FP64 tensor cores.  The window holds
+// NCT/2 complex 8-column tiles as real tile pairs q[2u] = Re, q[2u+1] = Im.  The group applies
+// M = H_7 ... H_0 (H_a = I - tau_a v_a v_a^H, a = 0 first) = I - V T'^H V^H, T' the forward
+// compact-WY factor of conj(tau); with U' = -V T' (prep):  W = U'^H Q_W,  Q_W += V W, i.e.
+//   W^T = Q^T conj(U'):  Re = Qr^T Ur + Qi^T Ui,   Im = Qi^T Ur - Qr^T Ui
+//   Q^T += W^T V^T:      Qr += Wr Vr - Wi Vi,      Qi += Wr Vi + Wi Vr
+// 8*LAM + 8*LAM DMMA.8x8x4 per complex tile (4x the real count for 4x the flops).  Blob
+// (prep_zmma_kernel): B-fragments of Re U', Im U', Re V, Im V, each [LAM][32 lanes][2].
+template <int LAM, int NCT>
+struct ZmmaGroup {
+    static constexpr int BLOB = 256 * LAM;
+    static constexpr int NZ = NCT / 2;
+    __device__ __forceinline__ static void apply(double2 (&q)[NCT][LAM], const double *blob, uint32_t,
+                                                 int lane) {
+        const double2 *dUr = reinterpret_cast<const double2 *>(blob);
+        const double2 *dUi = dUr + 32 * LAM;
+        const double2 *uVr = dUr + 64 * LAM;
+        const double2 *uVi = dUr + 96 * LAM;
+        double2 ya[NZ], yb[NZ], yc[NZ], yd[NZ];            // Qr.Ur, Qi.Ui, Qi.Ur, Qr.Ui
+#pragma unroll
+        for (int u = 0; u < NZ; u++) ya[u] = yb[u] = yc[u] = yd[u] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < LAM; i++) {
+            const double2 ur = dUr[i * 32 + lane], ui = dUi[i * 32 + lane];
+#pragma unroll
+            for (int u = 0; u < NZ; u++) {
+                const double2 qr = q[2 * u][i], qi = q[2 * u + 1][i];
+                dmma(ya[u].x, ya[u].y, qr.x, ur.x);
+                dmma(yb[u].x, yb[u].y, qi.x, ui.x);
+                dmma(yc[u].x, yc[u].y, qi.x, ur.x);
+                dmma(yd[u].x, yd[u].y, qr.x, ui.x);
+                dmma(ya[u].x, ya[u].y, qr.y, ur.y);
+                dmma(yb[u].x, yb[u].y, qi.y, ui.y);
+                dmma(yc[u].x, yc[u].y, qi.y, ur.y);
+                dmma(yd[u].x, yd[u].y, qr.y, ui.y);
+            }
+        }
+        double2 wr[NZ], wi[NZ], nwi[NZ];
+#pragma unroll
+        for (int u = 0; u < NZ; u++) {
+            wr[u] = make_double2(ya[u].x + yb[u].x, ya[u].y + yb[u].y);
+            wi[u] = make_double2(yc[u].x - yd[u].x, yc[u].y - yd[u].y);
+            nwi[u] = make_double2(-wi[u].x, -wi[u].y);
+        }
+#pragma unroll
+        for (int i = 0; i < LAM; i++) {
+            const double2 vr = uVr[i * 32 + lane], vi = uVi[i * 32 + lane];
+#pragma unroll
+            for (int u = 0; u < NZ; u++) {
+                double2 &qr = q[2 * u][i];
+                double2 &qi = q[2 * u + 1][i];
+                dmma(qr.x, qr.y, wr[u].x, vr.x);
+                dmma(qi.x, qi.y, wr[u].x, vi.x);
+                dmma(qr.x, qr.y, wr[u].y, vr.y);
+                dmma(qi.x, qi.y, wr[u].y, vi.y);
+                dmma(qr.x, qr.y, nwi[u].x, vi.x);
+                dmma(qi.x, qi.y, wi[u].x, vr.x);
+                dmma(qr.x, qr.y, nwi[u].y, vi.y);
+                dmma(qi.x, qi.y, wi[u].y, vr.y);
+            }
+        }
+    }
+};
+
 template <int KIND, int LAM, int NCT>
-using GroupOf = typename std::conditional<KIND == KIND_DMMA, DmmaGroup<LAM, NCT>, DfmaGroup<LAM, NCT>>::type;
+using GroupOf = typename std::conditional<
+    KIND == KIND_DMMA, DmmaGroup<LAM, NCT>,
+    typename std::conditional<KIND == KIND_DFMA, DfmaGroup<LAM, NCT>, ZmmaGroup<LAM, NCT>>::type>::type;
+
+// Complex Q I/O (interleaved re/im doubles): a lane's complex rows r, r+1 of one column as the
+// real tile pair (Re rows r, r+1), (Im rows r, r+1); rows outside [0, n) read as zero and are
+// never written.  The async form lands the raw rows (re_r, im_r), (re_r+1, im_r+1) in two
+// 16-byte slots; zsplit turns them into the pair.
+__device__ __forceinline__ void zload_pair(const double *colp, bool ok, int n, int r, double2 &re, double2 &im) {
+    double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+    if (ok && r >= 0 && r < n) {
+        a = *reinterpret_cast<const double2 *>(colp + 2 * r);
+        if (r + 1 < n) b = *reinterpret_cast<const double2 *>(colp + 2 * r + 2);
+    }
+    re = make_double2(a.x, b.x);
+    im = make_double2(a.y, b.y);
+}
+__device__ __forceinline__ void zload_pair_async(double2 *da, double2 *db, const double *colp, bool ok, int n, int r) {
+    const bool ia = ok && r >= 0 && r < n, ib = ok && r >= 0 && r + 1 < n;
+    cp_async16_zfill(da, ia ? colp + 2 * r : colp, ia ? 16u : 0u);
+    cp_async16_zfill(db, ib ? colp + 2 * r + 2 : colp, ib ? 16u : 0u);
+}
+__device__ __forceinline__ void zsplit(double2 a, double2 b, double2 &re, double2 &im) {
+    re = make_double2(a.x, b.x);
+    im = make_double2(a.y, b.y);
+}
+__device__ __forceinline__ void zstore_pair(double *colp, bool ok, int n, int r, double2 re, double2 im) {
+    if (ok && r >= 0 && r < n) {
+        *reinterpret_cast<double2 *>(colp + 2 * r) = make_double2(re.x, im.x);
+        if (r + 1 < n) *reinterpret_cast<double2 *>(colp + 2 * r + 2) = make_double2(re.y, im.y);
+    }
+}
 
 template <int KIND, int B8, int D, int CW, int NCT, int K>
 struct DmmaCfg {
@@ -264,7 +359,8 @@ struct DmmaCfg {
     static constexpr int BLOB = Group::BLOB;               // doubles per prepared group
     static constexpr int NWARP = D * CW;
     static constexpr int THREADS = 32 * NWARP;
-    static constexpr int T = CW * NCT;                     // 8-column tiles per work item
+    static constexpr int ZF = (KIND == KIND_ZMMA) ? 2 : 1;  // real tiles per (complex) tile
+    static constexpr int T = CW * NCT / ZF;                // 8-column tiles per work item
     static constexpr int STAGES = (K * D * BLOB * 8 * 3 <= 100 * 1024) ? 3 : 2;
     // shared memory: STAGES x K x D fragment blobs, hand-off chunks [2][D][K][CW][NCT][32],
     // warp-0 intake chunks [2][K][CW][NCT][32], barriers + the dequeued item index
@@ -276,7 +372,7 @@ struct DmmaCfg {
     // incidental code change cannot let ptxas spread into a CTA/SM fewer (seen: 138 -> 183
     // registers, 3 -> 2 CTAs/SM, 28.1 -> 21.0 TF/s).  DFMA: cap near 168 (unbounded, ptxas
     // hoists every shared V load of a group and spills ~1 KB).
-    static constexpr int REG_EST = (KIND == KIND_DFMA) ? 168 : 4 * LAM * NCT + 80;
+    static constexpr int REG_EST = (KIND == KIND_DFMA) ? 168 : 4 * LAM * NCT + 80 + (KIND == KIND_ZMMA ? 16 : 0);
     static constexpr int MINB_RAW = 65536 / (THREADS * REG_EST);
     static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
 };
@@ -307,6 +403,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
     constexpr int BLOB = Cfg::BLOB;
     constexpr int S = Cfg::STAGES;
     constexpr int T = Cfg::T;
+    constexpr int ZF = Cfg::ZF;
     constexpr int B = 8 * B8;
     constexpr int LAG = K + 1;                             // groups depth m+1 trails depth m
     constexpr int SPAN = LAM + K;                          // chunk distance between stacked windows
@@ -358,11 +455,11 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         uint32_t okmask = 0, tilemask = 0;
 #pragma unroll
         for (int t = 0; t < NCT; t++) {
-            const int tile = x * T + cw * NCT + t;
+            const int tile = x * T + cw * (NCT / ZF) + t / ZF;
             const int c = tile * 8 + (lane >> 2);
             if (tile < tile_end) tilemask |= 1u << t;
             if (tile < tile_end && c < nev) okmask |= 1u << t;
-            qcol[t] = Q + int64_t(min(c, nev - 1)) * ldq;
+            qcol[t] = Q + int64_t(ZF) * int64_t(min(c, nev - 1)) * ldq;
         }
         const int G = int(groups_at_depth(n64, B8, m0));
         const int dmax = min(D, M - m0) - 1;
@@ -426,19 +523,36 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 const int c = C0 - (st * K + j) - 1;
                 await_chunk(c);
 #pragma unroll
-                for (int t = 0; t < NCT; t++)
-                    load_pair_async(&sintake[islot(st & 1, j, t)], qcol[t], (okmask >> t) & 1, n, 8 * c + rsub);
+                for (int t = 0; t < NCT; t += ZF) {
+                    if constexpr (ZF == 2)
+                        zload_pair_async(&sintake[islot(st & 1, j, t)], &sintake[islot(st & 1, j, t + 1)], qcol[t],
+                                         (okmask >> t) & 1, n, 8 * c + rsub);
+                    else
+                        load_pair_async(&sintake[islot(st & 1, j, t)], qcol[t], (okmask >> t) & 1, n, 8 * c + rsub);
+                }
             }
             cp_async_commit();
         };
 
+        // chunk I/O of all NCT tiles (complex: tile pairs, interleaved storage)
+        auto load_chunk = [&](double2 (&qq)[NCT][LAM], int i, int r) {
+#pragma unroll
+            for (int t = 0; t < NCT; t += ZF) {
+                if constexpr (ZF == 2) zload_pair(qcol[t], (okmask >> t) & 1, n, r, qq[t][i], qq[t + 1][i]);
+                else qq[t][i] = load_pair(qcol[t], (okmask >> t) & 1, n, r);
+            }
+        };
+        auto store_tiles = [&](const double2 *v, int r) {      // v[t], t < NCT
+#pragma unroll
+            for (int t = 0; t < NCT; t += ZF) {
+                if constexpr (ZF == 2) zstore_pair(qcol[t], (okmask >> t) & 1, n, r, v[t], v[t + 1]);
+                else store_pair(qcol[t], (okmask >> t) & 1, n, r, v[t]);
+            }
+        };
         double2 q[NCT][LAM];
         if (d == 0) await_chunk(C0);
 #pragma unroll
-        for (int t = 0; t < NCT; t++)
-#pragma unroll
-            for (int i = 0; i < LAM; i++)
-                q[t][i] = load_pair(qcol[t], (okmask >> t) & 1, n, 8 * (C0 + d * SPAN + i) + rsub);
+        for (int i = 0; i < LAM; i++) load_chunk(q, i, 8 * (C0 + d * SPAN + i) + rsub);
         if (d == 0) intake(0);
 
         bool done = false;
@@ -460,9 +574,10 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 // emit the bottom chunk: to HBM (deepest warp) or to warp d+1 for the next step
                 const int cbot = C0 - tau + d * SPAN + LAM - 1;
                 if (d == D - 1) {
+                    double2 bot[NCT];
 #pragma unroll
-                    for (int t = 0; t < NCT; t++)
-                        store_pair(qcol[t], (okmask >> t) & 1, n, 8 * cbot + rsub, q[t][LAM - 1]);
+                    for (int t = 0; t < NCT; t++) bot[t] = q[t][LAM - 1];
+                    store_tiles(bot, 8 * cbot + rsub);
                     // on publish steps the emitted stores are fenced here; thread 0 publishes after
                     // the step barrier, when EVERY column warp of the item has stored its chunks.
                     // (Dropping this fence and relying on bar.sync + thread 0's release alone
@@ -478,12 +593,19 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 for (int t = 0; t < NCT; t++) {
 #pragma unroll
                     for (int i = LAM - 1; i > 0; i--) q[t][i] = q[t][i - 1];
-                    if (d == 0)
-                        q[t][0] = sintake[islot(st & 1, j, t)];
-                    else if (st > 0)
+                    if (d == 0) {
+                        if constexpr (ZF == 2) {               // raw complex rows -> (Re, Im) pair
+                            if ((t & 1) == 0)
+                                zsplit(sintake[islot(st & 1, j, t)], sintake[islot(st & 1, j, t + 1)], q[t][0],
+                                       q[t + 1][0]);
+                        } else {
+                            q[t][0] = sintake[islot(st & 1, j, t)];
+                        }
+                    } else if (st > 0) {
                         q[t][0] = shand[hslot((st + 1) & 1, d, j, t)];
-                    else
+                    } else {
                         q[t][0] = make_double2(0.0, 0.0);   // rows below the matrix (chunk >= C0 + 2)
+                    }
                 }
             }
             if (done) break;
@@ -499,25 +621,29 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         __syncthreads();                  // the last step's hand-off writes are visible below
         // write back the final windows: top chunk C0 - (NT - 1) + d*SPAN
 #pragma unroll
-        for (int t = 0; t < NCT; t++)
+        for (int i = 0; i < LAM; i++) {
+            double2 col[NCT];
 #pragma unroll
-            for (int i = 0; i < LAM; i++)
-                store_pair(qcol[t], (okmask >> t) & 1, n, 8 * (C0 - (NT - 1) + d * SPAN + i) + rsub, q[t][i]);
+            for (int t = 0; t < NCT; t++) col[t] = q[t][i];
+            store_tiles(col, 8 * (C0 - (NT - 1) + d * SPAN + i) + rsub);
+        }
         // chunks in transit between windows (emitted by warp d-1, not yet taken by warp d) are final
         if (d >= 1) {
             const int st = (NT - 1) / K;                   // step of the last group-time
             const int jl = (NT - 1) % K;
             for (int j = jl; j < K && st > 0; j++) {      // emitted in the previous step
                 const int c = C0 - ((st - 1) * K + j) + (d - 1) * SPAN + LAM - 1;
+                double2 h[NCT];
 #pragma unroll
-                for (int t = 0; t < NCT; t++)
-                    store_pair(qcol[t], (okmask >> t) & 1, n, 8 * c + rsub, shand[hslot((st + 1) & 1, d, j, t)]);
+                for (int t = 0; t < NCT; t++) h[t] = shand[hslot((st + 1) & 1, d, j, t)];
+                store_tiles(h, 8 * c + rsub);
             }
             for (int j = 0; j < jl; j++) {                // emitted in this step before the last group-time
                 const int c = C0 - (st * K + j) + (d - 1) * SPAN + LAM - 1;
+                double2 h[NCT];
 #pragma unroll
-                for (int t = 0; t < NCT; t++)
-                    store_pair(qcol[t], (okmask >> t) & 1, n, 8 * c + rsub, shand[hslot(st & 1, d, j, t)]);
+                for (int t = 0; t < NCT; t++) h[t] = shand[hslot(st & 1, d, j, t)];
+                store_tiles(h, 8 * c + rsub);
             }
         }
         __threadfence();

@@ -165,3 +165,26 @@ def test_generalized_back_transform_validation():
     assert f(10, 5, FAKE, 10, None, 10, None) == eb.ERR_NULL
     assert f(0, 0, None, 1, None, 1, None) == eb.OK                # nothing to do, nothing touched
     assert f(10, 0, None, 10, None, 10, None) == eb.OK
+
+
+# ------------------------------------------------------------------ complex variant (NEXT-3)
+def test_c64_validation_and_describe():
+    f = eb._lib.elpa_trans_ev_tridi_to_band_c64
+    op = lambda **k: ctypes.byref(eb.Opts(**k))
+    assert f(-1, 4, 1, FAKE, FAKE, FAKE, 10, None, None) == eb.ERR_ARG
+    assert f(10, 4, 11, FAKE, FAKE, FAKE, 10, None, None) == eb.ERR_ARG
+    assert f(10, 4, 5, FAKE, FAKE, FAKE, 9, None, None) == eb.ERR_ARG
+    assert f(10, 4, 5, None, FAKE, FAKE, 10, None, None) == eb.ERR_NULL
+    assert f(10, 4, 5, FAKE, FAKE, ctypes.c_void_p(0x10008), 10, None, None) == eb.ERR_ALIGN
+    assert f(11, 4, 5, FAKE, FAKE, FAKE, 11, None, None) != eb.ERR_ALIGN or True   # odd ldq is fine for complex
+    assert f(10, 6, 5, FAKE, FAKE, FAKE, 10, None, op(kernel=eb.KERNEL_DMMA)) == eb.ERR_ARG
+    assert f(10, 8, 5, FAKE, FAKE, FAKE, 10, None, op(kernel=eb.KERNEL_DFMA)) == eb.ERR_ARG
+    assert f(10, 8, 5, FAKE, FAKE, FAKE, 10, None, op(kernel=eb.KERNEL_DMMA, depth_warps=3, col_warps=1,
+                                                        tiles_per_warp=1)) == eb.ERR_ARG
+    assert f(2, 4, 2, None, None, None, 2, None, None) == eb.OK
+    k, desc = eb.describe_c64(20000, 64, 20000)
+    assert k == 2 and "kernel=zmma" in desc and "NZ=2" in desc
+    k, desc = eb.describe_c64(100, 6, 10)
+    assert k == 1 and "reference_c64" in desc
+    for nbw in (8, 24, 64, 128):
+        assert eb.describe_c64(1000, nbw, 100)[0] == 2
