@@ -593,14 +593,18 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 for (int t = 0; t < NCT; t++) {
 #pragma unroll
                     for (int i = LAM - 1; i > 0; i--) q[t][i] = q[t][i - 1];
-                    if (d == 0) {
-                        if constexpr (ZF == 2) {               // raw complex rows -> (Re, Im) pair
-                            if ((t & 1) == 0)
-                                zsplit(sintake[islot(st & 1, j, t)], sintake[islot(st & 1, j, t + 1)], q[t][0],
-                                       q[t + 1][0]);
-                        } else {
-                            q[t][0] = sintake[islot(st & 1, j, t)];
+                    if constexpr (ZF == 2) {
+                        // complex: tile t+1 is shifted in the next iteration, so the (Re, Im) pair
+                        // is split when its odd member is reached
+                        if (d == 0 && (t & 1)) {
+                            zsplit(sintake[islot(st & 1, j, t - 1)], sintake[islot(st & 1, j, t)], q[t - 1][0],
+                                   q[t][0]);
+                            continue;
                         }
+                        if (d == 0) continue;
+                    }
+                    if (d == 0) {
+                        q[t][0] = sintake[islot(st & 1, j, t)];
                     } else if (st > 0) {
                         q[t][0] = shand[hslot((st + 1) & 1, d, j, t)];
                     } else {

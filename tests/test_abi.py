@@ -183,7 +183,7 @@ def test_c64_validation_and_describe():
                                                         tiles_per_warp=1)) == eb.ERR_ARG
     assert f(2, 4, 2, None, None, None, 2, None, None) == eb.OK
     k, desc = eb.describe_c64(20000, 64, 20000)
-    assert k == 2 and "kernel=zmma" in desc and "NZ=2" in desc
+    assert k == 2 and "kernel=zmma" in desc and "CW=4 NZ=1" in desc
     k, desc = eb.describe_c64(100, 6, 10)
     assert k == 1 and "reference_c64" in desc
     for nbw in (8, 24, 64, 128):
