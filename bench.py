@@ -44,8 +44,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
-                    help="f32: the NEXT-3 single-precision variant (not the BASELINE metric)")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32", "c64"],
+                    help="f32 / c64: the NEXT-3 single-precision / complex Hermitian variants "
+                         "(not the BASELINE metric)")
     return ap.parse_args()
 
 
@@ -267,12 +268,76 @@ def run_f32(args):
     return 0
 
 
+def run_c64(args):
+    """--dtype c64: the complex Hermitian variant on the workload's shape
+    (1 GPU).  One step = one call of elpa_trans_ev_tridi_to_band_c64 (prep + apply).  Credited
+    16*nbw*nev flops per reflector (a complex multiply-add is 4 real ones)."""
+    import numpy as np
+    import torch
+    import paper_1811_01277_b200 as eb
+    from inputs import synthetic_reflectors_c, synthetic_q_c_np
+
+    dev = torch.device("cuda", 0)
+    n, nbw, nev = CONFIGS[args.config]
+    seed = config_seed(CFG_INDEX[args.config])
+    R = eb.hh_count(n, nbw)
+    hv, tau = synthetic_reflectors_c(R, nbw, seed)
+    dv, dt = torch.from_numpy(hv).to(dev), torch.from_numpy(tau).to(dev)
+    Q = torch.empty((nev, n), dtype=torch.complex128, device=dev)
+    for a in range(0, nev, 2000):
+        Q[a:a + 2000] = torch.from_numpy(synthetic_q_c_np(n, a, min(nev, a + 2000), seed)).to(dev)
+    cols = [0, nev - 1]
+    Q0 = Q[cols].clone()
+    nlaunch, desc = eb.describe_c64(n, nbw, nev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        eb.trans_ev_tridi_to_band(n, nbw, dv, dt, Q, stream=stream)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            eb.trans_ev_tridi_to_band(n, nbw, dv, dt, Q, stream=stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms_per_step = t0.elapsed_time(t1) / args.steps
+    flops = 16.0 * nbw * nev * R
+    value = flops / (ms_per_step * 1e-3) / 1e12
+    parity = None
+    if not args.no_cpu:
+        import oracle
+        Qt = Q0.clone()
+        eb.trans_ev_tridi_to_band(n, nbw, dv, dt, Qt, stream=stream)
+        torch.cuda.synchronize()
+        s_arr, L_arr = oracle.schedule(n, nbw)
+        want = oracle.apply_c(hv, tau, s_arr, L_arr, Q0.cpu().numpy())
+        got = Qt.cpu().numpy()
+        parity = float(np.abs(got - want).max() / np.abs(want).max())
+    peak = fp64_peak()["dmma"] or 36.98
+    print(json.dumps({
+        "metric": "trans_ev_tridi_to_band complex FP64 TFLOP/s (NEXT-3 variant; credited 16*nbw*nev per reflector)",
+        "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (complex recipe, inputs/synth.py)",
+        "config": {"workload": f"{args.config} n={n} nbw={nbw} nev={nev} complex", "n": n, "nbw": nbw, "nev": nev,
+                   "reflectors": R, "kernel": desc, "step": "prep+apply (one c64 call)",
+                   "l2": "inputs larger than L2 (Q %.2f GB, hh_v %.2f GB)" % (nev * n * 16 / 1e9, R * nbw * 16 / 1e9)},
+        "clocks": clk.summary(), "gpu_launches": nlaunch * args.steps,
+        "roofline": {"bound": "tensor", "achieved": value, "peak": peak, "unit": "TFLOP/s", "frac": value / peak,
+                     "traffic": None, "kernel": "apply_dmma_kernel<KIND_ZMMA> (+ prep_zmma_kernel: whole call timed)",
+                     "peak_source": "measured FP64 DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peaks_r01.jsonl)"},
+        "parity_max_rel_err_sampled": parity}))
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
     if args.dtype == "f32":
         return run_f32(args)
+    if args.dtype == "c64":
+        return run_c64(args)
 
     import numpy as np
     import torch
