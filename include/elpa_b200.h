@@ -30,9 +30,10 @@
  *   Q      : n x nev column-major with leading dimension ldq (eigenvector c = column c).
  *            In: eigenvectors of T.  Out: eigenvectors of B (same eigenvalues).  Updated
  *            in place; rows [n, ldq) of every column are never written.
- *   Ownership: the caller owns every buffer.  The library keeps no state between calls and
- *            no persistent allocation; the one-shot entry points take a temporary device
- *            workspace from cudaMallocAsync/cudaFreeAsync on `stream`.
+ *   Ownership: the caller owns every buffer.  The library keeps no problem state between calls.
+ *            The one-shot entry points take temporary device workspace, stream-ordered on
+ *            `stream`, from the library's own per-device memory pool, which keeps freed memory
+ *            cached for the next call (elpa_b200_release_cache returns it to the device).
  *   Concurrency: calls on distinct streams with distinct buffers may run concurrently (the
  *            analogue of ELPA's multiple instances).  No host synchronisation
  *            happens inside the device-pointer entry points.
@@ -89,6 +90,10 @@ typedef struct {
     int grid_ctas;       /* persistent CTAs to launch, 0 = all co-resident (148 x occupancy) */
     int groups_per_step; /* K: reflector groups (of 8) per CTA barrier (1,2,4), 0 = auto */
 } elpa_b200_opts;
+
+/* Return the memory the library's per-device pool caches between calls (temporary workspaces)
+ * to the device.  Call with no library work in flight on the current device.  OK or ERR_CUDA. */
+int elpa_b200_release_cache(void);
 
 /* R(n, nbw): number of reflectors the band->tridiagonal chase produces.
  * 0 if n < 3 or nbw == 1 (nbw = 1: the input is already tridiagonal);

@@ -25,6 +25,8 @@ def _load():
         _build.build()
     lib = ctypes.CDLL(_SO)
     i64, p, i32, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    lib.elpa_b200_release_cache.restype = i32
+    lib.elpa_b200_release_cache.argtypes = []
     lib.elpa_hh_count.restype = i64
     lib.elpa_hh_count.argtypes = [i64, i64]
     lib.elpa_trans_ev_tridi_to_band.restype = i32
@@ -97,6 +99,11 @@ class ElpaB200Error(RuntimeError):
 
 def strerror(code):
     return _lib.elpa_b200_strerror(int(code)).decode()
+
+
+def release_cache():
+    """Return the library's cached workspace memory to the device (elpa_b200_release_cache)."""
+    _check(_lib.elpa_b200_release_cache(), "elpa_b200_release_cache")
 
 
 def hh_count(n, nbw):

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -193,7 +194,7 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     uint64_t *prog = nullptr;
     // one progress word per work item + the work-item counter, zeroed per launch
     const size_t pbytes = size_t(p.items + 1) * 8;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
+    if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
     int rc = ELPA_B200_OK;
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
@@ -270,6 +271,14 @@ int apply_impl(const Plan &p, int64_t n, int64_t nbw, int64_t nev, const double 
 }  // namespace
 
 extern "C" {
+
+int elpa_b200_release_cache(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail_cuda();
+    cudaMemPool_t pool = lib_pool(dev);
+    if (pool && cudaMemPoolTrimTo(pool, 0) != cudaSuccess) return fail_cuda();
+    return ELPA_B200_OK;
+}
 
 int64_t elpa_hh_count(int64_t n, int64_t nbw) {
     if (n < 0 || nbw < 1) return -1;
@@ -353,7 +362,7 @@ int elpa_trans_ev_tridi_to_band_ex(int64_t n, int64_t nbw, int64_t nev, const do
     if ((rc = check_device()) != ELPA_B200_OK) return rc;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     void *ws = nullptr;
-    if (p.ws_bytes > 0 && cudaMallocAsync(&ws, size_t(p.ws_bytes), s) != cudaSuccess) return fail_cuda();
+    if (p.ws_bytes > 0 && lib_malloc_async(&ws, size_t(p.ws_bytes), s) != cudaSuccess) return fail_cuda();
     rc = prepare_impl(p, n, hh_v, hh_tau, ws, s);
     if (rc == ELPA_B200_OK) rc = apply_impl(p, n, nbw, nev, hh_v, hh_tau, ws, Q, ldq, s);
     if (ws && cudaFreeAsync(ws, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
@@ -376,6 +385,10 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     if (R == 0 || nev == 0) return ELPA_B200_OK;
     if ((rc = check_device()) != ELPA_B200_OK) return rc;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    using wall = std::chrono::steady_clock;
+    const auto w_enter = wall::now();
+    auto wall_ms = [&](wall::time_point t) { return std::chrono::duration<double, std::milli>(t - w_enter).count(); };
+    wall::time_point w_alloc = w_enter, w_enqueued = w_enter;
 
     // Column blocks of CH eigenvectors stream through NBUF device buffers: H2D on one copy
     // stream, apply on `stream`, D2H on another, so PCIe traffic overlaps the kernel (columns
@@ -387,35 +400,30 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t off_v = 0, off_t = up(bv), off_w = off_t + up(bt), off_q = off_w + up(size_t(p.ws_bytes));
     const size_t total = off_q + NBUF * up(bqc);
-    // Keep the transient buffers cached in the device's default pool between calls: with the
-    // default release threshold (0) every synchronising call would unmap and remap ~GBs.
-    {
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = 0, want = uint64_t(total);
-            if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess && thr < want)
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
-        }
-        cudaGetLastError();
-    }
     char *buf = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), total, s) != cudaSuccess) return fail_cuda();
+    if (lib_malloc_async(reinterpret_cast<void **>(&buf), total, s) != cudaSuccess) return fail_cuda();
+    w_alloc = wall::now();
     double *dv = reinterpret_cast<double *>(buf + off_v), *dt = reinterpret_cast<double *>(buf + off_t);
     void *ws = p.ws_bytes ? buf + off_w : nullptr;
     double *dq[NBUF];
     for (int i = 0; i < NBUF; i++) dq[i] = reinterpret_cast<double *>(buf + off_q + i * up(bqc));
 
-    cudaStream_t hs = nullptr, ds = nullptr;
+    cudaStream_t hs = nullptr, ds = nullptr, cs2 = nullptr;
     std::vector<cudaEvent_t> ev_h2d(nblk), ev_comp(nblk), ev_d2h(nblk);
-    cudaEvent_t ev_ready = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_prep = nullptr;
+    // ELPA_B200_TRACE=1: timed events, and one JSON line on stderr with every stage's completion
+    // time (ms after the buffer allocation): reflector upload + prep, per block H2D/apply/D2H
+    static const bool trace = getenv("ELPA_B200_TRACE") != nullptr;
+    const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
     bool ok = cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming) == cudaSuccess;
+              cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ev_ready, evflags) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ev_prep, evflags) == cudaSuccess;
     for (int64_t c = 0; ok && c < nblk; c++)
-        ok = cudaEventCreateWithFlags(&ev_h2d[c], cudaEventDisableTiming) == cudaSuccess &&
-             cudaEventCreateWithFlags(&ev_comp[c], cudaEventDisableTiming) == cudaSuccess &&
-             cudaEventCreateWithFlags(&ev_d2h[c], cudaEventDisableTiming) == cudaSuccess;
+        ok = cudaEventCreateWithFlags(&ev_h2d[c], evflags) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev_comp[c], evflags) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev_d2h[c], evflags) == cudaSuccess;
     if (!ok) rc = ELPA_B200_ERR_CUDA;
     // the buffer is allocated on `s`: the copy streams start after it
     if (rc == ELPA_B200_OK && (cudaEventRecord(ev_ready, s) != cudaSuccess ||
@@ -425,40 +433,71 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
                                cudaMemcpyAsync(dt, hh_tau, bt, cudaMemcpyHostToDevice, s) != cudaSuccess))
         rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) rc = prepare_impl(p, n, dv, dt, ws, s);
+    if (rc == ELPA_B200_OK && cudaEventRecord(ev_prep, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    // consecutive blocks alternate between `s` and a second compute stream, so the tail of one
+    // persistent launch (its last items, with SMs retiring) overlaps the start of the next
+    if (rc == ELPA_B200_OK && (cudaStreamWaitEvent(cs2, ev_prep, 0) != cudaSuccess)) rc = ELPA_B200_ERR_CUDA;
     for (int64_t c = 0; rc == ELPA_B200_OK && c < nblk; c++) {
         const int64_t c0 = c * CH, nc = std::min(CH, nev - c0);
         double *d = dq[c % NBUF];
+        cudaStream_t cs = (c & 1) ? cs2 : s;
         const size_t bytes = size_t(ldq) * nc * 8;
         if ((c >= NBUF && cudaStreamWaitEvent(hs, ev_d2h[c - NBUF], 0) != cudaSuccess) ||
             cudaMemcpyAsync(d, Q + c0 * ldq, bytes, cudaMemcpyHostToDevice, hs) != cudaSuccess ||
-            cudaEventRecord(ev_h2d[c], hs) != cudaSuccess || cudaStreamWaitEvent(s, ev_h2d[c], 0) != cudaSuccess) {
+            cudaEventRecord(ev_h2d[c], hs) != cudaSuccess || cudaStreamWaitEvent(cs, ev_h2d[c], 0) != cudaSuccess) {
             rc = ELPA_B200_ERR_CUDA;
             break;
         }
         Plan pc;
         if ((rc = make_plan(n, nbw, nc, opts, pc)) != ELPA_B200_OK) break;
-        if ((rc = apply_impl(pc, n, nbw, nc, dv, dt, ws, d, ldq, s)) != ELPA_B200_OK) break;
-        if (cudaEventRecord(ev_comp[c], s) != cudaSuccess || cudaStreamWaitEvent(ds, ev_comp[c], 0) != cudaSuccess ||
+        if ((rc = apply_impl(pc, n, nbw, nc, dv, dt, ws, d, ldq, cs)) != ELPA_B200_OK) break;
+        if (cudaEventRecord(ev_comp[c], cs) != cudaSuccess || cudaStreamWaitEvent(ds, ev_comp[c], 0) != cudaSuccess ||
             cudaMemcpyAsync(Q + c0 * ldq, d, bytes, cudaMemcpyDeviceToHost, ds) != cudaSuccess ||
             cudaEventRecord(ev_d2h[c], ds) != cudaSuccess) {
             rc = ELPA_B200_ERR_CUDA;
             break;
         }
     }
+    w_enqueued = wall::now();
     // everything (including work already queued when an error stopped the loop) completes
     // before the buffers go back to the pool
     if (ds) cudaStreamSynchronize(ds);
     if (hs) cudaStreamSynchronize(hs);
+    if (cs2) cudaStreamSynchronize(cs2);
     if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
     if (cudaStreamSynchronize(s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    if (trace && rc == ELPA_B200_OK) {
+        auto since = [&](cudaEvent_t e) {
+            float ms = -1.0f;
+            cudaEventElapsedTime(&ms, ev_ready, e);
+            return ms;
+        };
+        const double w_done = wall_ms(wall::now());
+        std::string line = "{\"elpa_b200_trace\": \"host_entry\", \"wall_alloc_ms\": " +
+                           std::to_string(wall_ms(w_alloc)) + ", \"wall_enqueued_ms\": " +
+                           std::to_string(wall_ms(w_enqueued)) + ", \"wall_done_ms\": " + std::to_string(w_done) +
+                           ", \"blocks\": " + std::to_string(nblk) +
+                           ", \"cols_per_block\": " + std::to_string(CH) + ", \"prep_done_ms\": " +
+                           std::to_string(since(ev_prep)) + ", \"h2d_ms\": [";
+        for (int64_t c = 0; c < nblk; c++) line += (c ? ", " : "") + std::to_string(since(ev_h2d[c]));
+        line += "], \"apply_ms\": [";
+        for (int64_t c = 0; c < nblk; c++) line += (c ? ", " : "") + std::to_string(since(ev_comp[c]));
+        line += "], \"d2h_ms\": [";
+        for (int64_t c = 0; c < nblk; c++) line += (c ? ", " : "") + std::to_string(since(ev_d2h[c]));
+        line += "]}\n";
+        fputs(line.c_str(), stderr);
+        cudaGetLastError();
+    }
     for (int64_t c = 0; c < nblk; c++) {
         if (ev_h2d[c]) cudaEventDestroy(ev_h2d[c]);
         if (ev_comp[c]) cudaEventDestroy(ev_comp[c]);
         if (ev_d2h[c]) cudaEventDestroy(ev_d2h[c]);
     }
     if (ev_ready) cudaEventDestroy(ev_ready);
+    if (ev_prep) cudaEventDestroy(ev_prep);
     if (hs) cudaStreamDestroy(hs);
     if (ds) cudaStreamDestroy(ds);
+    if (cs2) cudaStreamDestroy(cs2);
     if (rc != ELPA_B200_OK) cudaGetLastError();
     return rc;
 }
@@ -646,7 +685,7 @@ int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh
         if ((rc = make_plan(n, nbw, nev, &o, p)) != ELPA_B200_OK) break;
         const int kind = p.kernel == ELPA_B200_KERNEL_DFMA ? 1 : 0;
         if (p.kernel != ELPA_B200_KERNEL_REFERENCE && !ws[kind]) {
-            if (cudaMallocAsync(&ws[kind], size_t(p.ws_bytes), s) != cudaSuccess) {
+            if (lib_malloc_async(&ws[kind], size_t(p.ws_bytes), s) != cudaSuccess) {
                 rc = fail_cuda();
                 break;
             }
@@ -754,7 +793,7 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
     const size_t bW = size_t(P) * nev * 8;
     auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
     char *buf = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), up(bV) + 2 * up(bG) + 2 * up(bW), s) != cudaSuccess)
+    if (lib_malloc_async(reinterpret_cast<void **>(&buf), up(bV) + 2 * up(bG) + 2 * up(bW), s) != cudaSuccess)
         return fail_cuda();
     double *Vp = reinterpret_cast<double *>(buf), *G = reinterpret_cast<double *>(buf + up(bV));
     double *T = reinterpret_cast<double *>(buf + up(bV) + up(bG));
@@ -812,7 +851,7 @@ int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int
     const int64_t nb = (n + NB - 1) / NB;
     const size_t bInv = size_t(nb) * NB * NB * 8, bT = size_t(NB) * nev * 8;
     char *buf = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), ((bInv + 255) & ~size_t(255)) + bT, s) != cudaSuccess)
+    if (lib_malloc_async(reinterpret_cast<void **>(&buf), ((bInv + 255) & ~size_t(255)) + bT, s) != cudaSuccess)
         return fail_cuda();
     double *Linv = reinterpret_cast<double *>(buf), *T = reinterpret_cast<double *>(buf + ((bInv + 255) & ~size_t(255)));
     int dev = 0;

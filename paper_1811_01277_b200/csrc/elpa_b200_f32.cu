@@ -125,7 +125,7 @@ int f32_launch_shape(const F32Plan &p, int64_t n, int64_t nev, const float *ws, 
     if (grid > p.items) grid = p.items;
     uint64_t *prog = nullptr;
     const size_t pbytes = size_t(p.items + 1) * 8;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
+    if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
     int rc = ELPA_B200_OK;
     if (cudaMemsetAsync(prog, 0, pbytes, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
@@ -157,7 +157,7 @@ int f32_run(const F32Plan &p, int64_t n, int64_t nbw, int64_t nev, const float *
         return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
     }
     float *ws = nullptr;
-    if (p.ws_bytes > 0 && cudaMallocAsync(reinterpret_cast<void **>(&ws), size_t(p.ws_bytes), s) != cudaSuccess)
+    if (p.ws_bytes > 0 && lib_malloc_async(reinterpret_cast<void **>(&ws), size_t(p.ws_bytes), s) != cudaSuccess)
         return fail_cuda();
     int rc = ELPA_B200_ERR_ARG;
     switch (p.b8) {

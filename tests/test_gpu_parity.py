@@ -179,6 +179,11 @@ def test_host_entry_point(eb, n, nbw, nev):
     hq2 = torch.from_numpy(Q.copy())
     eb.trans_ev_tridi_to_band_host(n, nbw, torch.from_numpy(hv), torch.from_numpy(tau), hq2)
     assert np.array_equal(hq2.numpy(), dev)
+    # the library's cached workspace pool can be returned to the device, and calls still work
+    eb.release_cache()
+    hq3 = torch.from_numpy(Q.copy())
+    eb.trans_ev_tridi_to_band_host(n, nbw, torch.from_numpy(hv), torch.from_numpy(tau), hq3)
+    assert np.array_equal(hq3.numpy(), dev)
 
 
 def test_full_size_C3_sampled_columns(eb):
