@@ -52,6 +52,29 @@ __global__ void ffma2_kernel(float* out, float a, int iters) {
   if (s == 12345.678f) out[0] = s;
 }
 
+// the apply kernel's dot shape: acc_{k&1} += q_k * v_k with distinct pair registers q_k, v_k
+// (three distinct 64-bit operands per FFMA2), 4 accumulators
+template<int NQ>
+__global__ void ffma2_dot_kernel(float* out, float a, int iters) {
+  uint64_t q[NQ], v[NQ], acc[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < NQ; i++) {
+    float x = a + i * 1e-3f + threadIdx.x * 1e-7f;
+    q[i] = (uint64_t)__float_as_uint(x) | ((uint64_t)__float_as_uint(-x) << 32);
+    v[i] = (uint64_t)__float_as_uint(0.5f - i * 1e-4f) | ((uint64_t)__float_as_uint(0.25f) << 32);
+  }
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < NQ; i++) ffma2(acc[i & 3], q[i], v[i]);
+#pragma unroll
+    for (int i = 0; i < NQ; i++) q[i] ^= 0x8000000000000000ull;
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) s += __uint_as_float((uint32_t)acc[i]);
+  if (s == 12345.678f) out[0] = s;
+}
+
 template<typename K>
 float timeit(K launch, int reps) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -78,6 +101,13 @@ int main() {
     ms = timeit([&] { ffma2_kernel<16><<<blocks, threads>>>(out, 0.999f, iters); }, 5);
     fl = 4.0 * blocks * threads * 16.0 * iters;
     printf("{\"test\":\"ffma2_f32x2\",\"blocks_per_sm\":%d,\"threads\":%d,\"chains\":16,\"ms\":%.4f,\"tflops\":%.3f}\n",
+           bps, threads, ms, fl / ms / 1e9);
+  }
+  for (int bps : {2, 3, 4}) {
+    const int threads = 128, blocks = sms * bps;
+    float ms = timeit([&] { ffma2_dot_kernel<32><<<blocks, threads>>>(out, 0.999f, iters); }, 5);
+    double fl = 4.0 * blocks * threads * 32.0 * iters;
+    printf("{\"test\":\"ffma2_dot_3operand\",\"blocks_per_sm\":%d,\"threads\":%d,\"ms\":%.4f,\"tflops\":%.3f}\n",
            bps, threads, ms, fl / ms / 1e9);
   }
   CK(cudaDeviceSynchronize());
