@@ -749,7 +749,7 @@ const Cublas &cublas() {
     return c;
 }
 constexpr int kOpN = 0, kOpT = 1;
-constexpr int64_t kB2FPanel = 128;
+constexpr int64_t kB2FPanel = 256;
 
 // One cuBLAS handle per host thread and device, created on first use (handle creation costs
 // milliseconds; the handle carries no problem state), bound to stream s.  nullptr on failure;
