@@ -424,6 +424,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
     const int NX = (ntile + T - 1) / T;
     const int NP = (M + D - 1) / D;
     const int rsub = 2 * (lane & 3);
+    constexpr uint32_t kAllTiles = (1u << NCT) - 1u;
     // hand-off / intake slot of (parity, j, t) for this lane
     auto hslot = [&](int par, int dd, int j, int t) {
         return ((((par * D + dd) * K + j) * CW + cw) * NCT + t) * 32 + lane;
@@ -478,6 +479,10 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             const int g = G - 1 - tau + dd * LAG;
             return dd <= dmax && tau < NT && g >= 0 && g < G - dd * B8;
         };
+        // blob of group g at depth m0 + dd: bbase[dd] + g * BLOB (64-bit bases, once per item)
+        const double *bbase[D];
+#pragma unroll
+        for (int dd = 0; dd < D; dd++) bbase[dd] = blobs + group_base(n64, B8, m0 + dd) * BLOB;
         auto issue = [&](int st) {  // fragments of step st -> ring stage (stage0 + st) % S
             const int stg = (stage0 + st) % S;
             uint64_t *bar = &bars[stg];
@@ -490,8 +495,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 for (int dd = 0; dd <= dmax; dd++)
                     if (group_valid(st * K + j, dd)) {
                         const int g = G - 1 - (st * K + j) + dd * LAG;
-                        const double *src = blobs + (group_base(n64, B8, m0 + dd) + g) * BLOB;
-                        bulk_g2s(sblob + ((stg * K + j) * D + dd) * BLOB, src, BLOB * 8, bar);
+                        bulk_g2s(sblob + ((stg * K + j) * D + dd) * BLOB, bbase[dd] + int64_t(g) * BLOB, BLOB * 8, bar);
                     }
         };
         if (issuer)
@@ -522,13 +526,21 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             for (int j = 0; j < K; j++) {
                 const int c = C0 - (st * K + j) - 1;
                 await_chunk(c);
+                if (ZF == 1 && okmask == kAllTiles && c >= 0 && 8 * c + 8 <= n) {
+                    // interior chunk, every column valid: no bounds logic
 #pragma unroll
-                for (int t = 0; t < NCT; t += ZF) {
-                    if constexpr (ZF == 2)
-                        zload_pair_async(&sintake[islot(st & 1, j, t)], &sintake[islot(st & 1, j, t + 1)], qcol[t],
-                                         (okmask >> t) & 1, n, 8 * c + rsub);
-                    else
-                        load_pair_async(&sintake[islot(st & 1, j, t)], qcol[t], (okmask >> t) & 1, n, 8 * c + rsub);
+                    for (int t = 0; t < NCT; t++)
+                        cp_async16_zfill(&sintake[islot(st & 1, j, t)], qcol[t] + 8 * c + rsub, 16u);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < NCT; t += ZF) {
+                        if constexpr (ZF == 2)
+                            zload_pair_async(&sintake[islot(st & 1, j, t)], &sintake[islot(st & 1, j, t + 1)],
+                                             qcol[t], (okmask >> t) & 1, n, 8 * c + rsub);
+                        else
+                            load_pair_async(&sintake[islot(st & 1, j, t)], qcol[t], (okmask >> t) & 1, n,
+                                            8 * c + rsub);
+                    }
                 }
             }
             cp_async_commit();
@@ -543,6 +555,11 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             }
         };
         auto store_tiles = [&](const double2 *v, int r) {      // v[t], t < NCT
+            if (ZF == 1 && okmask == kAllTiles && r >= 0 && r + 2 <= n) {   // no bounds logic
+#pragma unroll
+                for (int t = 0; t < NCT; t++) *reinterpret_cast<double2 *>(qcol[t] + r) = v[t];
+                return;
+            }
 #pragma unroll
             for (int t = 0; t < NCT; t += ZF) {
                 if constexpr (ZF == 2) zstore_pair(qcol[t], (okmask >> t) & 1, n, r, v[t], v[t + 1]);
