@@ -330,8 +330,22 @@ def run_c64(args):
     return 0
 
 
+def _private_stdout():
+    """The contract's stdout is ONE JSON line.  Libraries write banners to fd 1 on their own (NCCL
+    prints "NCCL version ..." when the environment asks for it): point fd 1 at stderr and keep a
+    private duplicate of the real stdout for this script's print()."""
+    try:
+        sys.stdout.flush()
+        fd = os.dup(1)
+        os.dup2(2, 1)
+        sys.stdout = os.fdopen(fd, "w", buffering=1)
+    except OSError:
+        pass
+
+
 def main():
     args = parse()
+    _private_stdout()
     if args.impl == "reference":
         return reference_arm(args)
     if args.dtype == "f32":
