@@ -19,8 +19,13 @@
 //        Q_W^T += W^T V_g^T            2*lambda MMAs (K = reflectors)           [rank-8 update, a6]
 //     The dot accumulator layout is directly the update's A-operand layout (K index permuted
 //     to match), so no shuffles are needed anywhere.
-//   * Prepared fragments of the D groups of the next step are fetched with cp.async.bulk
-//     into a 2-stage shared-memory ring completed on an mbarrier (one elected thread).
+//   * Prepared fragments of the D groups of a step are fetched ahead with cp.async.bulk into
+//     a 2-3 stage shared-memory ring completed on mbarriers, issued by one thread of the last
+//     warp (warp 0 already carries the HBM intake, the item dequeue and the progress publish).
+//   * Interior chunks (inside the matrix, every column valid) take a load/store fast path
+//     without bounds logic; only the first/last chunks and the last tile group pay for it.
+//   * KIND_ZMMA runs complex Hermitian tiles (NEXT-3) as (Re, Im) real tile pairs, and
+//     KIND_DFMA the same groups on the FP64 CUDA cores (the measured alternative).
 #pragma once
 #include <type_traits>
 
