@@ -57,7 +57,8 @@ typedef struct CUstream_st *elpa_b200_stream_t;
 
 enum {
     ELPA_B200_OK = 0,
-    ELPA_B200_ERR_ARG = -1,    /* n < 0, nbw < 1, nev < 0, nev > n, ldq < max(1,n), bad opts */
+    ELPA_B200_ERR_ARG = -1,    /* n < 0 or n > 2^31 - 64, nbw < 1, nev < 0, nev > n, ldq < max(1,n),
+                                  bad opts */
     ELPA_B200_ERR_NULL = -2,   /* a required pointer is NULL (R > 0 and nev > 0) */
     ELPA_B200_ERR_ALIGN = -3,  /* Q not 16-byte aligned, ldq odd (FP64) / not a multiple of 4 (FP32);
                                   workspace not 256-byte aligned */

@@ -147,7 +147,7 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
 
 int validate(int64_t n, int64_t nbw, int64_t nev, const void *hh_v, const void *hh_tau, const void *Q,
              int64_t ldq, bool check_q_align) {
-    if (n < 0 || nbw < 1 || nev < 0 || nev > n || ldq < (n > 1 ? n : 1)) return ELPA_B200_ERR_ARG;
+    if (n < 0 || nbw < 1 || nev < 0 || nev > n || ldq < (n > 1 ? n : 1) || n > kMaxN) return ELPA_B200_ERR_ARG;
     const int64_t R = hh_total(n, nbw);
     if (R > 0 && nev > 0 && (!hh_v || !hh_tau || !Q)) return ELPA_B200_ERR_NULL;
     if (check_q_align && R > 0 && nev > 0 && ((ldq & 1) || (reinterpret_cast<uintptr_t>(Q) & 15)))

@@ -12,6 +12,8 @@
 namespace elpa_b200_host {
 
 constexpr int kMaxSms = 148;
+// The kernels index rows and chunks with 32-bit integers (row 8c + 7 < 2^31).
+constexpr int64_t kMaxN = (int64_t(1) << 31) - 64;
 
 inline int sm_count() {
     int dev = 0, n = kMaxSms;

@@ -72,6 +72,7 @@ def test_validation_order_before_device():
     assert _call(10, 4, -1, FAKE, FAKE, FAKE, 10) == eb.ERR_ARG         # nev < 0
     assert _call(10, 4, 11, FAKE, FAKE, FAKE, 10) == eb.ERR_ARG         # nev > n
     assert _call(10, 4, 5, FAKE, FAKE, FAKE, 9) == eb.ERR_ARG           # ldq < n
+    assert _call(1 << 31, 4, 5, FAKE, FAKE, FAKE, 1 << 31) == eb.ERR_ARG   # beyond 32-bit row indexing
     assert _call(10, 4, 5, None, FAKE, FAKE, 10) == eb.ERR_NULL
     assert _call(10, 4, 5, FAKE, None, FAKE, 10) == eb.ERR_NULL
     assert _call(10, 4, 5, FAKE, FAKE, None, 10) == eb.ERR_NULL
