@@ -176,12 +176,26 @@ int elpa_b200_autotune_progress(const elpa_b200_autotune *at, int *tried, int *t
 int64_t elpa_b200_autotune_save(const elpa_b200_autotune *at, char *buf, size_t buflen);
 elpa_b200_autotune *elpa_b200_autotune_load(const char *state, int *error);
 void elpa_b200_autotune_destroy(elpa_b200_autotune *at);
+/* The same tuning for the NEXT-3 variants (element type ELPA_B200_DTYPE_*).  FAST: the variant's
+ * fast kernel with its automatic shape (and its reference kernel for small problems); MEDIUM
+ * adds every compiled shape of the variant (FP32: D, CW, NC, K; complex: D, CW, complex tiles).
+ * elpa_b200_autotune_setup == _setup_dtype(..., ELPA_B200_DTYPE_F64, ...).  Snapshots carry the
+ * type (format v2; v1 snapshots load as FP64). */
+enum { ELPA_B200_DTYPE_F64 = 0, ELPA_B200_DTYPE_F32 = 1, ELPA_B200_DTYPE_C64 = 2 };
+elpa_b200_autotune *elpa_b200_autotune_setup_dtype(int64_t n, int64_t nbw, int64_t nev, int level, int dtype,
+                                                  int *error);
 /* Convenience: run the whole loop on device buffers.  Prepares the reflectors once per kernel
  * variant, times each candidate's apply on Q (which is overwritten: pass a scratch copy) with
  * CUDA events on `stream` (best of `reps`), returns the best options and time. */
 int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
                            double *Q_scratch, int64_t ldq, elpa_b200_stream_t stream, int level, int reps,
                            elpa_b200_opts *best, double *best_ms);
+
+/* The loop for any element type: hh_v, hh_tau, Q_scratch point to data of that type (complex:
+ * interleaved doubles).  FP32 and complex candidates are timed as whole calls (prep + apply). */
+int elpa_b200_autotune_run_dtype(int64_t n, int64_t nbw, int64_t nev, int dtype, const void *hh_v, const void *hh_tau,
+                                 void *Q_scratch, int64_t ldq, elpa_b200_stream_t stream, int level, int reps,
+                                 elpa_b200_opts *best, double *best_ms);
 
 /* ---------------------------------------------------------------------------------------
  * NEXT-1: band -> full back-transformation (the second transform of every eigenvector in the

@@ -75,6 +75,11 @@ def _load():
     lib.elpa_b2f_count.argtypes = [i64, i64]
     lib.elpa_trans_ev_band_to_full.restype = i32
     lib.elpa_trans_ev_band_to_full.argtypes = [i64, i64, i64, p, i64, p, p, i64, p]
+    lib.elpa_b200_autotune_setup_dtype.restype = p
+    lib.elpa_b200_autotune_setup_dtype.argtypes = [i64, i64, i64, i32, i32, pi]
+    lib.elpa_b200_autotune_run_dtype.restype = i32
+    lib.elpa_b200_autotune_run_dtype.argtypes = [i64, i64, i64, i32, p, p, p, i64, p, i32, i32, p,
+                                                 ctypes.POINTER(ctypes.c_double)]
     lib.elpa_b200_autotune_run.restype = i32
     lib.elpa_b200_autotune_run.argtypes = [i64, i64, i64, p, p, p, i64, p, i32, i32, p, ctypes.POINTER(ctypes.c_double)]
     return lib
@@ -274,6 +279,7 @@ def credited_flops(n, nbw, nev):
 
 
 AUTOTUNE_FAST, AUTOTUNE_MEDIUM = 1, 2
+DTYPE_F64, DTYPE_F32, DTYPE_C64 = 0, 1, 2
 
 
 def opts_dict(o):
@@ -291,12 +297,13 @@ class Autotuner:
 
     save() / Autotuner.load(state) snapshot and resume the loop."""
 
-    def __init__(self, n=None, nbw=None, nev=None, level=AUTOTUNE_FAST, _handle=None):
+    def __init__(self, n=None, nbw=None, nev=None, level=AUTOTUNE_FAST, _handle=None, dtype=DTYPE_F64):
         if _handle is None:
             err = ctypes.c_int(0)
-            _handle = _lib.elpa_b200_autotune_setup(int(n), int(nbw), int(nev), int(level), ctypes.byref(err))
+            _handle = _lib.elpa_b200_autotune_setup_dtype(int(n), int(nbw), int(nev), int(level), int(dtype),
+                                                          ctypes.byref(err))
             if not _handle:
-                raise ElpaB200Error(err.value, "elpa_b200_autotune_setup")
+                raise ElpaB200Error(err.value, "elpa_b200_autotune_setup_dtype")
         self._h = ctypes.c_void_p(_handle)
 
     def __del__(self):
@@ -340,15 +347,21 @@ class Autotuner:
 
 
 def autotune(n, nbw, hh_v, hh_tau, Q_scratch, level=AUTOTUNE_MEDIUM, reps=2, stream=None):
-    """Run the autotuning loop on device buffers (elpa_b200_autotune_run); Q_scratch is
-    overwritten.  Returns (best opts dict, best apply time in ms)."""
+    """Run the autotuning loop on device buffers (elpa_b200_autotune_run[_dtype]); Q_scratch is
+    overwritten.  The element type follows Q_scratch (float64, float32 or complex128).  Returns
+    (best opts dict, best time in ms: the apply for float64, the whole call otherwise)."""
+    import torch
     nev, ldq = _q_ldq(Q_scratch)
     o, ms = Opts(), ctypes.c_double(0)
     s = _stream_handle(stream, Q_scratch.device)
-    rc = _lib.elpa_b200_autotune_run(int(n), int(nbw), int(nev), _dev_ptr(hh_v, "hh_v"), _dev_ptr(hh_tau, "hh_tau"),
-                                     _dev_ptr(Q_scratch, "Q"), int(ldq), s, int(level), int(reps), ctypes.byref(o),
-                                     ctypes.byref(ms))
-    _check(rc, "elpa_b200_autotune_run")
+    dt = {torch.float64: DTYPE_F64, torch.float32: DTYPE_F32, torch.complex128: DTYPE_C64}.get(Q_scratch.dtype)
+    if dt is None:
+        raise TypeError("Q_scratch must be float64, float32 or complex128")
+    tdt = Q_scratch.dtype
+    rc = _lib.elpa_b200_autotune_run_dtype(int(n), int(nbw), int(nev), dt, _dev_ptr(hh_v, "hh_v", tdt),
+                                           _dev_ptr(hh_tau, "hh_tau", tdt), _dev_ptr(Q_scratch, "Q", tdt), int(ldq), s,
+                                           int(level), int(reps), ctypes.byref(o), ctypes.byref(ms))
+    _check(rc, "elpa_b200_autotune_run_dtype")
     return opts_dict(o), ms.value
 
 

@@ -511,6 +511,7 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
 struct elpa_b200_autotune {
     int64_t n = 0, nbw = 0, nev = 0;
     int level = 0;
+    int dtype = ELPA_B200_DTYPE_F64;
     std::vector<elpa_b200_opts> cand;
     std::vector<double> ms;       // reported time per candidate (< 0: not yet)
     int next = 0;                 // index the next _step returns
@@ -518,6 +519,40 @@ struct elpa_b200_autotune {
 };
 
 namespace {
+std::vector<elpa_b200_opts> autotune_candidates_variant(int64_t n, int64_t nbw, int64_t nev, int level, int dtype) {
+    // FP32 / complex: FAST = the variant's fast kernel (automatic shape) and, for small problems,
+    // its reference kernel; MEDIUM adds every compiled shape of the variant's menu
+    std::vector<elpa_b200_opts> c;
+    const int fast = dtype == ELPA_B200_DTYPE_F32 ? ELPA_B200_KERNEL_FFMA2 : ELPA_B200_KERNEL_DMMA;
+    const bool ok = nbw % 8 == 0 && nbw >= 8 && nbw <= 128;
+    elpa_b200_opts o{};
+    if (ok) {
+        o.kernel = fast;
+        c.push_back(o);
+    }
+    if (!ok || double(hh_total(n, nbw)) * double(nev) * double(nbw) < 2e9) {
+        o = elpa_b200_opts{};
+        o.kernel = ELPA_B200_KERNEL_REFERENCE;
+        c.push_back(o);
+    }
+    if (level >= ELPA_B200_AUTOTUNE_MEDIUM && ok) {
+        int menu[64][4];
+        const int cnt = dtype == ELPA_B200_DTYPE_F32 ? f32_shape_menu(int(nbw / 8), menu, 64)
+                                                     : c64_shape_menu(int(nbw / 8), menu, 64);
+        char buf[8];
+        for (int i = 0; i < cnt; i++) {
+            o = elpa_b200_opts{};
+            o.kernel = fast;
+            o.depth_warps = menu[i][0]; o.col_warps = menu[i][1]; o.tiles_per_warp = menu[i][2];
+            o.groups_per_step = menu[i][3];
+            const int r = dtype == ELPA_B200_DTYPE_F32 ? elpa_b200_describe_f32(n, nbw, nev, &o, buf, sizeof buf)
+                                                       : elpa_b200_describe_c64(n, nbw, nev, &o, buf, sizeof buf);
+            if (r >= 0) c.push_back(o);
+        }
+    }
+    return c;
+}
+
 std::vector<elpa_b200_opts> autotune_candidates(int64_t n, int64_t nbw, int64_t nev, int level) {
     std::vector<elpa_b200_opts> c;
     auto mk = [](int kernel, int D, int CW, int NCT) {
@@ -556,18 +591,25 @@ std::vector<elpa_b200_opts> autotune_candidates(int64_t n, int64_t nbw, int64_t 
 
 extern "C" {
 
-elpa_b200_autotune *elpa_b200_autotune_setup(int64_t n, int64_t nbw, int64_t nev, int level, int *error) {
+elpa_b200_autotune *elpa_b200_autotune_setup_dtype(int64_t n, int64_t nbw, int64_t nev, int level, int dtype,
+                                                  int *error) {
     if (error) *error = ELPA_B200_OK;
     if (n < 0 || nbw < 1 || nev < 0 || nev > n ||
-        (level != ELPA_B200_AUTOTUNE_FAST && level != ELPA_B200_AUTOTUNE_MEDIUM)) {
+        (level != ELPA_B200_AUTOTUNE_FAST && level != ELPA_B200_AUTOTUNE_MEDIUM) ||
+        (dtype != ELPA_B200_DTYPE_F64 && dtype != ELPA_B200_DTYPE_F32 && dtype != ELPA_B200_DTYPE_C64)) {
         if (error) *error = ELPA_B200_ERR_ARG;
         return nullptr;
     }
     auto *at = new elpa_b200_autotune;
-    at->n = n; at->nbw = nbw; at->nev = nev; at->level = level;
-    at->cand = autotune_candidates(n, nbw, nev, level);
+    at->n = n; at->nbw = nbw; at->nev = nev; at->level = level; at->dtype = dtype;
+    at->cand = dtype == ELPA_B200_DTYPE_F64 ? autotune_candidates(n, nbw, nev, level)
+                                            : autotune_candidates_variant(n, nbw, nev, level, dtype);
     at->ms.assign(at->cand.size(), -1.0);
     return at;
+}
+
+elpa_b200_autotune *elpa_b200_autotune_setup(int64_t n, int64_t nbw, int64_t nev, int level, int *error) {
+    return elpa_b200_autotune_setup_dtype(n, nbw, nev, level, ELPA_B200_DTYPE_F64, error);
 }
 
 int elpa_b200_autotune_step(elpa_b200_autotune *at, elpa_b200_opts *opts) {
@@ -608,9 +650,9 @@ int elpa_b200_autotune_progress(const elpa_b200_autotune *at, int *tried, int *t
 
 int64_t elpa_b200_autotune_save(const elpa_b200_autotune *at, char *buf, size_t buflen) {
     if (!at) return ELPA_B200_ERR_NULL;
-    std::string st = "elpa_b200_autotune v1 " + std::to_string(at->n) + " " + std::to_string(at->nbw) + " " +
-                     std::to_string(at->nev) + " " + std::to_string(at->level) + " " + std::to_string(at->next) +
-                     " " + std::to_string(at->cand.size());
+    std::string st = "elpa_b200_autotune v2 " + std::to_string(at->n) + " " + std::to_string(at->nbw) + " " +
+                     std::to_string(at->nev) + " " + std::to_string(at->level) + " " + std::to_string(at->dtype) +
+                     " " + std::to_string(at->next) + " " + std::to_string(at->cand.size());
     char tmp[64];
     for (double v : at->ms) {
         snprintf(tmp, sizeof tmp, " %.17g", v);
@@ -628,12 +670,14 @@ elpa_b200_autotune *elpa_b200_autotune_load(const char *state, int *error) {
         return nullptr;
     }
     long long n, nbw, nev;
-    int level, next, cnt, used = 0;
-    if (sscanf(state, "elpa_b200_autotune v1 %lld %lld %lld %d %d %d%n", &n, &nbw, &nev, &level, &next, &cnt,
-               &used) != 6)
+    int level, next, cnt, used = 0, dtype = ELPA_B200_DTYPE_F64;
+    if (sscanf(state, "elpa_b200_autotune v2 %lld %lld %lld %d %d %d %d%n", &n, &nbw, &nev, &level, &dtype, &next,
+               &cnt, &used) != 7 &&
+        sscanf(state, "elpa_b200_autotune v1 %lld %lld %lld %d %d %d%n", &n, &nbw, &nev, &level, &next, &cnt,
+               &used) != 6)   // v1 snapshots (FP64 only) still load
         return nullptr;
     int err = 0;
-    elpa_b200_autotune *at = elpa_b200_autotune_setup(n, nbw, nev, level, &err);
+    elpa_b200_autotune *at = elpa_b200_autotune_setup_dtype(n, nbw, nev, level, dtype, &err);
     if (!at) return nullptr;
     if (int(at->cand.size()) != cnt || next < 0 || next > cnt) {   // a different build's menu
         delete at;
@@ -654,6 +698,59 @@ elpa_b200_autotune *elpa_b200_autotune_load(const char *state, int *error) {
 }
 
 void elpa_b200_autotune_destroy(elpa_b200_autotune *at) { delete at; }
+
+int elpa_b200_autotune_run_dtype(int64_t n, int64_t nbw, int64_t nev, int dtype, const void *hh_v, const void *hh_tau,
+                                 void *Q_scratch, int64_t ldq, elpa_b200_stream_t stream, int level, int reps,
+                                 elpa_b200_opts *best, double *best_ms) {
+    if (dtype == ELPA_B200_DTYPE_F64)
+        return elpa_b200_autotune_run(n, nbw, nev, static_cast<const double *>(hh_v),
+                                      static_cast<const double *>(hh_tau), static_cast<double *>(Q_scratch), ldq,
+                                      stream, level, reps, best, best_ms);
+    if (!best) return ELPA_B200_ERR_NULL;
+    if (reps < 1) reps = 1;
+    int err = 0;
+    elpa_b200_autotune *at = elpa_b200_autotune_setup_dtype(n, nbw, nev, level, dtype, &err);
+    if (!at) return err;
+    auto call = [&](const elpa_b200_opts *o) {
+        return dtype == ELPA_B200_DTYPE_F32
+                   ? elpa_trans_ev_tridi_to_band_f32(n, nbw, nev, static_cast<const float *>(hh_v),
+                                                     static_cast<const float *>(hh_tau), static_cast<float *>(Q_scratch),
+                                                     ldq, stream, o)
+                   : elpa_trans_ev_tridi_to_band_c64(n, nbw, nev, static_cast<const double *>(hh_v),
+                                                     static_cast<const double *>(hh_tau),
+                                                     static_cast<double *>(Q_scratch), ldq, stream, o);
+    };
+    int rc = call(nullptr);                          // validation (and a warm-up) through the entry point
+    if (rc != ELPA_B200_OK || hh_total(n, nbw) == 0 || nev == 0) {
+        if (rc == ELPA_B200_OK) {
+            elpa_b200_autotune_step(at, best);
+            if (best_ms) *best_ms = 0.0;
+        }
+        elpa_b200_autotune_destroy(at);
+        return rc;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) rc = fail_cuda();
+    elpa_b200_opts o;
+    while (rc == ELPA_B200_OK && elpa_b200_autotune_step(at, &o) == 1) {
+        float bestv = 1e30f;
+        for (int r = 0; r < reps && rc == ELPA_B200_OK; r++) {   // whole call: prep + apply
+            cudaEventRecord(e0, s);
+            rc = call(&o);
+            cudaEventRecord(e1, s);
+            if (rc == ELPA_B200_OK && cudaEventSynchronize(e1) != cudaSuccess) rc = fail_cuda();
+            float ms = 0.f;
+            if (rc == ELPA_B200_OK && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess && ms < bestv) bestv = ms;
+        }
+        if (rc == ELPA_B200_OK) elpa_b200_autotune_report(at, bestv > 0.f ? bestv : 1e-6);
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (rc == ELPA_B200_OK) rc = elpa_b200_autotune_best(at, best, best_ms);
+    elpa_b200_autotune_destroy(at);
+    return rc;
+}
 
 int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
                            double *Q, int64_t ldq, elpa_b200_stream_t stream, int level, int reps,

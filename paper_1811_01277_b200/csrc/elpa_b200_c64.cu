@@ -171,6 +171,19 @@ int z_run(const ZPlan &p, int64_t n, int64_t nbw, int64_t nev, const double *hh_
 
 }  // namespace
 
+int elpa_b200_host::c64_shape_menu(int b8, int (*out)[4], int max) {
+    int k = 0;
+    auto add = [&](const ZShape *sh, int cnt) {
+        for (int i = 0; i < cnt && k < max; i++, k++) {
+            out[k][0] = sh[i].D; out[k][1] = sh[i].CW; out[k][2] = sh[i].NZ; out[k][3] = 1;
+        }
+    };
+    if (!z_b8_supported(8 * int64_t(b8))) return 0;
+    if (z_full_menu(b8)) add(kZShapes, int(sizeof(kZShapes) / sizeof(kZShapes[0])));
+    else add(kZSmallShapes, int(sizeof(kZSmallShapes) / sizeof(kZSmallShapes[0])));
+    return k;
+}
+
 extern "C" {
 
 int elpa_trans_ev_tridi_to_band_c64(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,

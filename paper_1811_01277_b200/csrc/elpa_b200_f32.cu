@@ -177,6 +177,19 @@ int f32_run(const F32Plan &p, int64_t n, int64_t nbw, int64_t nev, const float *
 
 }  // namespace
 
+int elpa_b200_host::f32_shape_menu(int b8, int (*out)[4], int max) {
+    int k = 0;
+    auto add = [&](const F32Shape *sh, int cnt) {
+        for (int i = 0; i < cnt && k < max; i++, k++) {
+            out[k][0] = sh[i].D; out[k][1] = sh[i].CW; out[k][2] = sh[i].NC; out[k][3] = sh[i].K;
+        }
+    };
+    if (!f32_b8_supported(8 * int64_t(b8))) return 0;
+    if (f32_full_menu(b8)) add(kF32Shapes, int(sizeof(kF32Shapes) / sizeof(kF32Shapes[0])));
+    else add(kF32SmallShapes, int(sizeof(kF32SmallShapes) / sizeof(kF32SmallShapes[0])));
+    return k;
+}
+
 extern "C" {
 
 int elpa_trans_ev_tridi_to_band_f32(int64_t n, int64_t nbw, int64_t nev, const float *hh_v, const float *hh_tau,

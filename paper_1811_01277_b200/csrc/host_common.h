@@ -90,4 +90,9 @@ inline cudaError_t lib_malloc_async(void **p, size_t bytes, cudaStream_t s) {
     return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
+// Compiled shape menus of the FP32 and complex translation units for a given b8 (autotuning):
+// writes up to `max` shapes as {D, CW, tiles_per_warp, groups_per_step}, returns the count.
+int f32_shape_menu(int b8, int (*out)[4], int max);
+int c64_shape_menu(int b8, int (*out)[4], int max);
+
 }  // namespace elpa_b200_host

@@ -60,3 +60,33 @@ def test_errors():
         at.report(-1.0)
     with pytest.raises(eb.ElpaB200Error):
         eb.Autotuner.load("garbage")
+
+
+def test_variant_candidates_and_snapshot():
+    """NEXT-2 over the NEXT-3 variants: FP32 / complex menus, MEDIUM > FAST, v2 snapshots keep the type"""
+    for dt, fast_kernel in ((eb.DTYPE_F32, eb.KERNEL_FFMA2), (eb.DTYPE_C64, eb.KERNEL_DMMA)):
+        fast = eb.Autotuner(20000, 64, 20000, eb.AUTOTUNE_FAST, dtype=dt)
+        med = eb.Autotuner(20000, 64, 20000, eb.AUTOTUNE_MEDIUM, dtype=dt)
+        assert fast.progress()[1] == 1 and med.progress()[1] > 3
+        o = fast.step()
+        assert o["kernel"] == fast_kernel and o["depth_warps"] == 0
+        shapes = []
+        while (x := med.step()) is not None:
+            shapes.append((x["kernel"], x["depth_warps"], x["col_warps"], x["tiles_per_warp"], x["groups_per_step"]))
+            med.report(10.0 + len(shapes))
+        assert len(set(shapes)) == len(shapes)
+        st = med.save()
+        assert st.startswith("elpa_b200_autotune v2 ") and f" {dt} " in st
+        again = eb.Autotuner.load(st)
+        assert again.best() == med.best()
+    small = eb.Autotuner(300, 16, 40, eb.AUTOTUNE_FAST, dtype=eb.DTYPE_C64)
+    kinds = []
+    while (x := small.step()) is not None:
+        kinds.append(x["kernel"])
+    assert kinds == [eb.KERNEL_DMMA, eb.KERNEL_REFERENCE]
+    # v1 snapshots (FP64 only) still load
+    v1 = eb.Autotuner(300, 16, 40, eb.AUTOTUNE_FAST).save().replace(" v2 ", " v1 ").split()
+    del v1[6]                                              # the v2 dtype field
+    assert eb.Autotuner.load(" ".join(v1)).progress() == eb.Autotuner(300, 16, 40, eb.AUTOTUNE_FAST).progress()
+    with pytest.raises(eb.ElpaB200Error):
+        eb.Autotuner(300, 16, 40, eb.AUTOTUNE_FAST, dtype=7)

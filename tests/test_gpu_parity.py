@@ -388,3 +388,34 @@ def test_two_stage_pipeline_on_gpu(eb, n, nbw, nev):
     assert _rel(got, c["Qfull"]) <= TOL
     A, X, lam = c["A"], got.T, c["lam"]
     assert np.linalg.norm(A @ X - X * lam) / (n * np.linalg.norm(A)) <= 1e-13
+
+
+@pytest.mark.parametrize("dtype", ["float32", "complex128"])
+def test_autotune_variants_run_and_use_best(eb, dtype):
+    """NEXT-2 over the NEXT-3 variants: the runner times every candidate; its best options give
+    parity (FP32: R14 tolerance; complex: 1e-12)"""
+    import torch
+    from inputs import synthetic_reflectors_c, synthetic_q_c_np
+    n, nbw, nev = 600, 32, 96
+    s, L = oracle.schedule(n, nbw)
+    if dtype == "float32":
+        hv, tau = synthetic_reflectors(len(s), nbw, 71)
+        Q = synthetic_q_np(n, 0, nev, 71, ldq=n)
+        hv, tau, Q = hv.astype(np.float32), tau.astype(np.float32), Q.astype(np.float32)
+        want = oracle.apply(hv.astype(np.float64), tau.astype(np.float64), s, L, Q.astype(np.float64))
+    else:
+        hv, tau = synthetic_reflectors_c(len(s), nbw, 71)
+        Q = synthetic_q_c_np(n, 0, nev, 71)
+        want = oracle.apply_c(hv, tau, s, L, Q)
+    dv, dt = torch.from_numpy(hv).cuda(), torch.from_numpy(tau).cuda()
+    best, ms = eb.autotune(n, nbw, dv, dt, torch.from_numpy(Q.copy()).cuda(), level=eb.AUTOTUNE_MEDIUM, reps=1)
+    assert ms > 0
+    dq = torch.from_numpy(Q.copy()).cuda()
+    eb.trans_ev_tridi_to_band(n, nbw, dv, dt, dq, opts=best)
+    torch.cuda.synchronize()
+    got = dq.cpu().numpy()
+    if dtype == "float32":
+        err = (np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)).max()
+        assert err <= 8 * 2.0 ** -24 * np.sqrt(n * nbw / 2)
+    else:
+        assert _rel(got, want) <= TOL
