@@ -44,6 +44,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -418,7 +421,15 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
     double2 *shand = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS);                    // [2][D][K][CW][NCT][32]
     double2 *sintake = reinterpret_cast<double2 *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND);  // [2][K][CW][NCT][32]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + Cfg::SMEM_BLOBS + Cfg::SMEM_HAND + Cfg::SMEM_INTAKE);
-    int *s_item = reinterpret_cast<int *>(bars + S);
+    uint64_t *ebars = bars + S;                            // per-stage "consumed" barriers (ring mode)
+    int *s_item = reinterpret_cast<int *>(bars + 2 * S);
+    // Ring mode (one depth warp row, one group per step, 3+ stages): no CTA barrier per step.
+    // Every warp arrives on the stage's "consumed" mbarrier after its group; the issuer refills a
+    // stage only after all warps consumed its previous use, one step of slack behind (fragments
+    // are issued AHEAD = S-2 steps ahead).  CTA barriers remain on publish steps (progress words)
+    // and at item boundaries.
+    constexpr bool kRing = (D == 1 && K == 1 && S >= 3);
+    constexpr int AHEAD = kRing ? S - 2 : S - 1;
 
     const int n = int(n64), nev = int(nev64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -441,12 +452,14 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; i++) mbar_init(&bars[i], 1);
+        for (int i = 0; i < S; i++) mbar_init(&ebars[i], D * CW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     uint32_t phase_bits = 0;  // parity of the next completion, per stage (all threads track it)
     int stage0 = 0;           // ring stage of the item's step 0
+    int gstep0 = 0;           // global step index of the item's step 0 (ring mode)
 
     for (;;) {
         if (threadIdx.x == 0)
@@ -491,6 +504,10 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         auto issue = [&](int st) {  // fragments of step st -> ring stage (stage0 + st) % S
             const int stg = (stage0 + st) % S;
             uint64_t *bar = &bars[stg];
+            if constexpr (kRing) {                          // previous use of this stage consumed?
+                const int g = gstep0 + st;
+                if (g >= S) mbar_wait(&ebars[stg], uint32_t(((g / S) - 1) & 1));
+            }
             uint32_t bytes = 0;
             for (int j = 0; j < K; j++)
                 for (int dd = 0; dd <= dmax; dd++)
@@ -504,7 +521,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                     }
         };
         if (issuer)
-            for (int st = 0; st < S - 1 && st < nsteps; st++) issue(st);
+            for (int st = 0; st < AHEAD && st < nsteps; st++) issue(st);
 
         // cross-pass dependency (warp 0 only): chunk c must be final from pass p-1
         uint32_t seen = 0;
@@ -579,7 +596,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
 
         bool done = false;
         for (int st = 0; !done; st++) {
-            if (issuer && st + S - 1 < nsteps) issue(st + S - 1);
+            if (issuer && st + AHEAD < nsteps) issue(st + AHEAD);
             if (d == 0 && st + 1 < nsteps) intake(st + 1);
             const uint32_t stage = uint32_t((stage0 + st) % S);
             const uint32_t par = (phase_bits >> stage) & 1u;
@@ -591,6 +608,10 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 if (group_valid(tau, d)) {
                     if (!waited) { mbar_wait(&bars[stage], par); waited = true; }
                     Cfg::Group::apply(q, sblob + ((stage * K + j) * D + d) * BLOB, tilemask, lane);
+                }
+                if constexpr (kRing) {                      // this warp is done with the stage
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&ebars[stage]);
                 }
                 if (tau + 1 >= NT) { done = true; break; }     // final windows written back below
                 // emit the bottom chunk: to HBM (deepest warp) or to warp d+1 for the next step
@@ -635,7 +656,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 }
             }
             if (done) break;
-            __syncthreads();
+            if (!kRing || pub_step(st)) __syncthreads();
             if (threadIdx.x == 0 && pub_step(st)) {
                 // every chunk >= the deepest warps' last emission is final for the next pass
                 const int cbot = C0 - (st * K + K - 1) + (D - 1) * SPAN + LAM - 1;
@@ -676,6 +697,7 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         __syncthreads();  // item complete: publish, and the smem ring/hand-off are free again
         if (threadIdx.x == 0) st_release_u64(prog + k, kPassDone);
         stage0 = (stage0 + nsteps) % S;
+        gstep0 += nsteps;
     }
 }
 
