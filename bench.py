@@ -10,7 +10,9 @@ C3 (n = 20000, nbw = 64, nev = 20000), the north-star target configuration.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the deliberately slow
-plain C program in oracle/) on a bounded column sample of the same workload.
+plain C program in oracle/) on a bounded column sample of the same workload.  In the GPU arms the
+oracle is used only by the cpu_baseline legs (cpu_baseline_leg_*): the timed CPU baseline and the
+sampled parity of the run's columns.
 """
 import argparse
 import json
@@ -153,6 +155,77 @@ def reference_arm(args):
     return 0
 
 
+def cpu_baseline_leg_f64(n, nbw, nev, R, seed, world, c0, nev_loc, hh_v, hh_tau, Q, total_apps, config):
+    """The cpu_baseline leg of the FP64 arm: (1) at N = 1, the CPU oracle timed on a column sample of
+    the workload (cpu_baseline); (2) the oracle recomputes 3 columns of this run after its
+    `total_apps` applications (sampled parity).  Returns (cpu_baseline dict or None, parity)."""
+    import numpy as np
+    import oracle
+    cpu = None
+    if world == 1:
+        r, dt, thr, nc = cpu_oracle_rate(n, nbw, nev, seed, 256 if R * nbw < 5e8 else 32,
+                                         hh=(hh_v.cpu().numpy(), hh_tau.cpu().numpy()))
+        cpu = {"value": r, "unit": UNIT, "cores": thr, "kind": "oracle",
+               "sample": f"{nc} evenly spaced columns of {config} (all {R} reflectors), {dt:.1f} s"}
+    cols = [0, nev_loc // 2, nev_loc - 1]
+    s_arr, L_arr = oracle.schedule(n, nbw)
+    Qs = np.concatenate([synthetic_q_np(n, c0 + c, c0 + c + 1, seed) for c in cols])
+    step_r = 1 << 22                      # stream the reflectors from the device in chunks
+    for _ in range(total_apps):
+        for r1 in range(R, 0, -step_r):
+            r0 = max(0, r1 - step_r)
+            Qs = oracle.apply(hh_v[r0:r1].cpu().numpy(), hh_tau[r0:r1].cpu().numpy(), s_arr[r0:r1],
+                              L_arr[r0:r1], Qs)
+    got = Q[cols].cpu().numpy()
+    return cpu, float(np.abs(got - Qs).max() / np.abs(Qs).max())
+
+
+def cpu_baseline_leg_f32(eb, n, nbw, R, nev_loc, hh_v, hh_tau, Q0, stream, config):
+    """The cpu_baseline leg of the FP32 line: the fp64 CPU oracle, timed, on 2 columns of a fresh
+    call from the same FP32 inputs; their column-wise error is the sampled parity (R14)."""
+    import numpy as np
+    import torch
+    import oracle
+    cols = [0, nev_loc - 1]
+    Qt = Q0[cols].clone()
+    eb.trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Qt, stream=stream)
+    torch.cuda.synchronize()
+    s_arr, L_arr = oracle.schedule(n, nbw)
+    want = Q0[cols].double().cpu().numpy()
+    step_r = 1 << 22
+    t = 0.0
+    for r1 in range(R, 0, -step_r):
+        r0 = max(0, r1 - step_r)
+        hv, ht = hh_v[r0:r1].double().cpu().numpy(), hh_tau[r0:r1].double().cpu().numpy()
+        t0 = time.perf_counter()
+        want = oracle.apply(hv, ht, s_arr[r0:r1], L_arr[r0:r1], want)
+        t += time.perf_counter() - t0
+    got = Qt.double().cpu().numpy()
+    parity = float((np.linalg.norm(got[:, :n] - want[:, :n], axis=1) / np.linalg.norm(want[:, :n], axis=1)).max())
+    cpu = {"value": 4.0 * nbw * len(cols) * R / t / 1e12, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+           "sample": f"{len(cols)} columns of {config} (all {R} reflectors, fp64 oracle), {t:.1f} s"}
+    return cpu, parity
+
+
+def cpu_baseline_leg_c64(eb, n, nbw, R, hv, tau, dv, dt, Q0, stream, config):
+    """The cpu_baseline leg of the complex line: the CPU oracle (oracle_apply_c), timed, on the 2
+    sampled columns of a fresh call; max relative error is the sampled parity."""
+    import numpy as np
+    import torch
+    import oracle
+    Qt = Q0.clone()
+    eb.trans_ev_tridi_to_band(n, nbw, dv, dt, Qt, stream=stream)
+    torch.cuda.synchronize()
+    s_arr, L_arr = oracle.schedule(n, nbw)
+    t0 = time.perf_counter()
+    want = oracle.apply_c(hv, tau, s_arr, L_arr, Q0.cpu().numpy())
+    t = time.perf_counter() - t0
+    got = Qt.cpu().numpy()
+    cpu = {"value": 16.0 * nbw * Q0.shape[0] * R / t / 1e12, "unit": UNIT, "cores": os.cpu_count(),
+           "kind": "oracle", "sample": f"{Q0.shape[0]} columns of {config} complex (all {R} reflectors), {t:.1f} s"}
+    return cpu, float(np.abs(got - want).max() / np.abs(want).max())
+
+
 def run_f32(args):
     """--dtype f32: the FP32 variant on the same workload, inputs rounded
     to FP32 once.  One step = [N>1: NCCL broadcast of the FP32 reflectors] + one call of
@@ -219,24 +292,9 @@ def run_f32(args):
     flops_total = 4.0 * nbw * nev * R
     value = flops_total / (ms_per_step * 1e-3) / 1e12
 
-    parity = None
+    cpu, parity = None, None
     if rank == 0 and not args.no_cpu:
-        # the oracle (fp64) recomputes 2 columns of a fresh single call from the same FP32 inputs
-        import oracle
-        cols = [0, nev_loc - 1]
-        Qt = Q0[cols].clone()
-        eb.trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Qt, stream=stream)
-        torch.cuda.synchronize()
-        s_arr, L_arr = oracle.schedule(n, nbw)
-        want = Q0[cols].double().cpu().numpy()
-        step_r = 1 << 22
-        for r1 in range(R, 0, -step_r):
-            r0 = max(0, r1 - step_r)
-            want = oracle.apply(hh_v[r0:r1].double().cpu().numpy(), hh_tau[r0:r1].double().cpu().numpy(),
-                                s_arr[r0:r1], L_arr[r0:r1], want)
-        got = Qt.double().cpu().numpy()
-        parity = float((np.linalg.norm(got[:, :n] - want[:, :n], axis=1) /
-                        np.linalg.norm(want[:, :n], axis=1)).max())
+        cpu, parity = cpu_baseline_leg_f32(eb, n, nbw, R, nev_loc, hh_v, hh_tau, Q0, stream, args.config)
 
     peak = None
     try:
@@ -262,7 +320,7 @@ def run_f32(args):
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "apply_f32_kernel (+ prep_f32_kernel: whole call timed)",
                          "peak_source": "measured packed FP32 FMA (fma.rn.f32x2) peak on this pool's B200 (profiles/fp32_peaks_r01.jsonl)"},
-            "parity_colwise_rel_err_sampled": parity}))
+            "cpu_baseline": cpu, "parity_colwise_rel_err_sampled": parity}))
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -303,16 +361,9 @@ def run_c64(args):
     ms_per_step = t0.elapsed_time(t1) / args.steps
     flops = 16.0 * nbw * nev * R
     value = flops / (ms_per_step * 1e-3) / 1e12
-    parity = None
+    cpu, parity = None, None
     if not args.no_cpu:
-        import oracle
-        Qt = Q0.clone()
-        eb.trans_ev_tridi_to_band(n, nbw, dv, dt, Qt, stream=stream)
-        torch.cuda.synchronize()
-        s_arr, L_arr = oracle.schedule(n, nbw)
-        want = oracle.apply_c(hv, tau, s_arr, L_arr, Q0.cpu().numpy())
-        got = Qt.cpu().numpy()
-        parity = float(np.abs(got - want).max() / np.abs(want).max())
+        cpu, parity = cpu_baseline_leg_c64(eb, n, nbw, R, hv, tau, dv, dt, Q0, stream, args.config)
     peak = fp64_peak()["dmma"] or 36.98
     print(json.dumps({
         "metric": "trans_ev_tridi_to_band complex FP64 TFLOP/s (NEXT-3 variant; credited 16*nbw*nev per reflector)",
@@ -326,7 +377,7 @@ def run_c64(args):
         "roofline": {"bound": "tensor", "achieved": value, "peak": peak, "unit": "TFLOP/s", "frac": value / peak,
                      "traffic": None, "kernel": "apply_dmma_kernel<KIND_ZMMA> (+ prep_zmma_kernel: whole call timed)",
                      "peak_source": "measured FP64 DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peaks_r01.jsonl)"},
-        "parity_max_rel_err_sampled": parity}))
+        "cpu_baseline": cpu, "parity_max_rel_err_sampled": parity}))
     return 0
 
 
@@ -428,22 +479,12 @@ def main():
     flops_total = 4.0 * nbw * nev * R                    # all ranks together (credited)
     value = flops_total / (ms_per_step * 1e-3) / 1e12
 
-    # ---- sampled parity at full size (rank 0): oracle recomputes a few columns of this run
-    parity = None
+    # ---- the cpu_baseline leg (rank 0): the CPU oracle, timed on a column sample (N = 1), and the
+    # sampled parity of this run's columns
+    cpu, parity = None, None
     if rank == 0 and not args.no_cpu:
-        import oracle
-        total_apps = args.warmup + args.steps
-        cols = [0, nev_loc // 2, nev_loc - 1]
-        s_arr, L_arr = oracle.schedule(n, nbw)
-        Qs = np.concatenate([synthetic_q_np(n, c0 + c, c0 + c + 1, seed) for c in cols])
-        step_r = 1 << 22                      # stream the reflectors from the device in chunks
-        for _ in range(total_apps):
-            for r1 in range(R, 0, -step_r):
-                r0 = max(0, r1 - step_r)
-                Qs = oracle.apply(hh_v[r0:r1].cpu().numpy(), hh_tau[r0:r1].cpu().numpy(), s_arr[r0:r1],
-                                  L_arr[r0:r1], Qs)
-        got = Q[cols].cpu().numpy()
-        parity = float(np.abs(got - Qs).max() / np.abs(Qs).max())
+        cpu, parity = cpu_baseline_leg_f64(n, nbw, nev, R, seed, world, c0, nev_loc, hh_v, hh_tau, Q,
+                                           args.warmup + args.steps, args.config)
 
     # ---- end to end through the host-buffer C-ABI entry point (pinned host memory)
     e2e = None
@@ -488,13 +529,6 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "kernel": "apply_dmma_kernel",
                 "peak_source": "measured FP64 DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peaks_r01.jsonl)",
                 "apply_ms": apply_avg, "exact_flops_frac": None}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        r, dt, thr, nc = cpu_oracle_rate(n, nbw, nev, seed, 256 if R * nbw < 5e8 else 32,
-                                         hh=(hh_v.cpu().numpy(), hh_tau.cpu().numpy()))
-        cpu = {"value": r, "unit": UNIT, "cores": thr, "kind": "oracle",
-               "sample": f"{nc} evenly spaced columns of {args.config} (all {R} reflectors), {dt:.1f} s"}
 
     if rank == 0:
         out = {
