@@ -1,4 +1,5 @@
-"""Small cases for compute-sanitizer runs (memcheck / racecheck / synccheck), one process."""
+"""Small cases for compute-sanitizer runs (memcheck / racecheck / synccheck), one process; kept under
+tests/ because it checks results against the oracle.  Not collected by pytest (no test_ prefix)."""
 import sys
 import numpy as np
 import torch
