@@ -116,7 +116,7 @@ int elpa_trans_ev_tridi_to_band_ex(int64_t n, int64_t nbw, int64_t nev,
 
 /* Host-buffer call (end-to-end path): hh_v, hh_tau, Q are HOST pointers (pinned memory is
  * needed for copy/compute overlap).  Copies the reflectors to a temporary device workspace on
- * `stream` and prepares them, then streams Q through the GPU in ~8 column blocks (H2D, apply,
+ * `stream` and prepares them, then streams Q through the GPU in ~6 column blocks (H2D, apply,
  * D2H on two internal copy streams, overlapped with the kernel), and synchronises before
  * returning.  The result is bitwise that of the device-pointer call. */
 int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev,

@@ -393,7 +393,14 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     // Column blocks of CH eigenvectors stream through NBUF device buffers: H2D on one copy
     // stream, apply on `stream`, D2H on another, so PCIe traffic overlaps the kernel (columns
     // are independent: each block's result is bitwise the unblocked one).
-    const int64_t CH = std::max<int64_t>(8, ((nev + 7) / 8 + 7) / 8 * 8);   // ~8 blocks
+    // ~6 column blocks (measured 4/6/8/12 at C3: 645/645/648/664 ms; profiles/host_blocks_r01.log;
+    // development override: ELPA_B200_HOST_BLOCKS)
+    static const int64_t kBlocks = [] {
+        const char *e = getenv("ELPA_B200_HOST_BLOCKS");
+        const int64_t v = e ? atoll(e) : 6;
+        return v >= 1 ? v : 6;
+    }();
+    const int64_t CH = std::max<int64_t>(8, ((nev + kBlocks - 1) / kBlocks + 7) / 8 * 8);
     const int64_t nblk = (nev + CH - 1) / CH;
     constexpr int NBUF = 3;
     const size_t bqc = size_t(ldq) * CH * 8, bv = size_t(R) * nbw * 8, bt = size_t(R) * 8;
