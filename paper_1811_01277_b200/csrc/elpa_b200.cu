@@ -101,7 +101,10 @@ void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int
     //                 C2    C4    C3/8  C3/4  C3    C5/8
     //   (1,2,4,1)   17.8  24.8  25.8  27.1  28.1  27.7
     //   (2,2,2,1)   19.4  25.7  26.6  27.4  27.7  27.5
+    // MEDIUM autotuning with the final kernel (profiles/autotune_medium_r01_final.jsonl): C3 keeps
+    // (1,2,4,1) 28.7, C4 keeps (2,2,2,1) 26.1, C2 (nbw = 32) prefers (4,2,2,1) 22.3 over 21.2
     if (b8 == 8 && ntile >= 2000) { D = 1; CW = 2; NCT = 4; }
+    else if (b8 == 4 && ntile < 2000) { D = 4; CW = 2; NCT = 2; }
     else { D = 2; CW = 2; NCT = 2; }   // also the default of the small menu (nbw != 8/16/32/64)
 }
 

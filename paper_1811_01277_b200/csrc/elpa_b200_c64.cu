@@ -73,10 +73,10 @@ int z_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, ZP
     p.b8 = int(nbw / 8);
     int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NZ = o ? o->tiles_per_warp : 0;
     if (D == 0 && CW == 0 && NZ == 0) {
-        // measured (profiles/next3_c64_shape_sweep_r01.jsonl, TF/s credited): C3 (1,4,1) 30.2,
-        // (2,2,2) 27.0; C2 (1,4,1) 22.6, (2,2,2) 19.7; C4 (2,2,2) 22.7, (1,4,1) 14.3
-        if (z_full_menu(p.b8) && (nev + 7) / 8 >= 400) { D = 1; CW = 4; NZ = 1; }
-        else if (z_full_menu(p.b8)) { D = 2; CW = 2; NZ = 2; }
+        // (1,4,1) everywhere on the full menu: MEDIUM autotuning with the ring-mode kernel
+        // (profiles/autotune_medium_r01_final.jsonl) picks it at C4 (28.2 TF/s; (2,2,2) measured
+        // 22.1) and keeps the automatic choice at C2; C3 (1,4,1) 30.7
+        if (z_full_menu(p.b8)) { D = 1; CW = 4; NZ = 1; }
         else { D = 2; CW = 2; NZ = 1; }
     }
     if (!z_shape_compiled(p.b8, D, CW, NZ)) return ELPA_B200_ERR_ARG;
