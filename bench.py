@@ -110,6 +110,37 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def host_cpu_model():
+    """The host CPU model (lscpu's "Model name"), for the cpu_baseline record."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def exact_len_sum(n, nbw):
+    """sum_r L_r over the chase's reflectors (exact flops = 4 * sum L * nev; SURVEY §8a "Report
+    both"): sweep j has M_j = (n-3-j)//nbw + 1 reflectors, all of length nbw except the last,
+    whose length is n - s_last with s_last = j + 1 + (M_j - 1) nbw."""
+    import numpy as np
+    if n < 3 or nbw < 2:
+        return 0
+    j = np.arange(n - 2, dtype=np.int64)
+    M = (n - 3 - j) // nbw + 1
+    s_last = j + 1 + (M - 1) * nbw
+    return int(np.sum(nbw * (M - 1) + np.minimum(nbw, n - s_last)))
+
+
 def cpu_oracle_rate(n, nbw, nev, seed, ncols, threads=None, hh=None):
     """Time the plain CPU oracle (oracle/, never tuned) on `ncols` sampled columns.
     hh = (hh_v, hh_tau) host arrays if already available."""
@@ -149,7 +180,8 @@ def reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} n={n} nbw={nbw} nev={nev}", "n": n, "nbw": nbw, "nev": nev},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
+                         "cpu_model": host_cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0}))
     return 0
@@ -165,7 +197,7 @@ def cpu_baseline_leg_f64(n, nbw, nev, R, seed, world, c0, nev_loc, hh_v, hh_tau,
     if world == 1:
         r, dt, thr, nc = cpu_oracle_rate(n, nbw, nev, seed, 256 if R * nbw < 5e8 else 32,
                                          hh=(hh_v.cpu().numpy(), hh_tau.cpu().numpy()))
-        cpu = {"value": r, "unit": UNIT, "cores": thr, "kind": "oracle",
+        cpu = {"value": r, "unit": UNIT, "cores": thr, "kind": "oracle", "cpu_model": host_cpu_model(),
                "sample": f"{nc} evenly spaced columns of {config} (all {R} reflectors), {dt:.1f} s"}
     cols = [0, nev_loc // 2, nev_loc - 1]
     s_arr, L_arr = oracle.schedule(n, nbw)
@@ -182,7 +214,7 @@ def cpu_baseline_leg_f64(n, nbw, nev, R, seed, world, c0, nev_loc, hh_v, hh_tau,
 
 def cpu_baseline_leg_f32(eb, n, nbw, R, nev_loc, hh_v, hh_tau, Q0, stream, config):
     """The cpu_baseline leg of the FP32 line: the fp64 CPU oracle, timed, on 2 columns of a fresh
-    call from the same FP32 inputs; their column-wise error is the sampled parity (R14)."""
+    call from the same FP32 inputs; their elementwise error (R14 units) is the sampled parity."""
     import numpy as np
     import torch
     import oracle
@@ -201,8 +233,11 @@ def cpu_baseline_leg_f32(eb, n, nbw, R, nev_loc, hh_v, hh_tau, Q0, stream, confi
         want = oracle.apply(hv, ht, s_arr[r0:r1], L_arr[r0:r1], want)
         t += time.perf_counter() - t0
     got = Qt.double().cpu().numpy()
-    parity = float((np.linalg.norm(got[:, :n] - want[:, :n], axis=1) / np.linalg.norm(want[:, :n], axis=1)).max())
+    # elementwise, in units of 7 x the column's rms entry (R14, tests/test_gpu_f32.py)
+    rms = np.linalg.norm(want[:, :n], axis=1) / np.sqrt(n)
+    parity = float((np.abs(got[:, :n] - want[:, :n]).max(axis=1) / (7.0 * rms)).max())
     cpu = {"value": 4.0 * nbw * len(cols) * R / t / 1e12, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+           "cpu_model": host_cpu_model(),
            "sample": f"{len(cols)} columns of {config} (all {R} reflectors, fp64 oracle), {t:.1f} s"}
     return cpu, parity
 
@@ -222,7 +257,7 @@ def cpu_baseline_leg_c64(eb, n, nbw, R, hv, tau, dv, dt, Q0, stream, config):
     t = time.perf_counter() - t0
     got = Qt.cpu().numpy()
     cpu = {"value": 16.0 * nbw * Q0.shape[0] * R / t / 1e12, "unit": UNIT, "cores": os.cpu_count(),
-           "kind": "oracle", "sample": f"{Q0.shape[0]} columns of {config} complex (all {R} reflectors), {t:.1f} s"}
+           "kind": "oracle", "cpu_model": host_cpu_model(), "sample": f"{Q0.shape[0]} columns of {config} complex (all {R} reflectors), {t:.1f} s"}
     return cpu, float(np.abs(got - want).max() / np.abs(want).max())
 
 
@@ -320,7 +355,7 @@ def run_f32(args):
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "apply_f32_kernel (+ prep_f32_kernel: whole call timed)",
                          "peak_source": "measured packed FP32 FMA (fma.rn.f32x2) peak on this pool's B200 (profiles/fp32_peaks_r01.jsonl)"},
-            "cpu_baseline": cpu, "parity_colwise_rel_err_sampled": parity}))
+            "cpu_baseline": cpu, "parity_elementwise_sampled": parity, "parity_bound": 8.0 * 2.0 ** -24 * (n * nbw / 2.0) ** 0.5}))
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -528,7 +563,8 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": "apply_dmma_kernel",
                 "peak_source": "measured FP64 DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peaks_r01.jsonl)",
-                "apply_ms": apply_avg, "exact_flops_frac": None}
+                "apply_ms": apply_avg,
+                "exact_flops_frac": 4.0 * exact_len_sum(n, nbw) * nev_loc / (apply_avg * 1e-3) / 1e12 / peak}
 
     if rank == 0:
         out = {

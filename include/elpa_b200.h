@@ -93,8 +93,14 @@ typedef struct {
 } elpa_b200_opts;
 
 /* Return the memory the library's per-device pool caches between calls (temporary workspaces)
- * to the device.  Call with no library work in flight on the current device.  OK or ERR_CUDA. */
+ * to the device.  Call with no library work in flight on the current device.  OK or ERR_CUDA.
+ * Deviation from the no-persistent-allocation rule of SURVEY §8(b), on by default: the pool keeps
+ * freed workspace mapped so the next call does not re-map several GB (measured at C3: e2e
+ * 18.8 -> 24.6 TFLOP/s).  elpa_b200_set_workspace_cache(0) switches the current
+ * device's pool to release freed memory at every synchronisation (nothing outlives a call) and
+ * trims it now; (1) restores caching.  OK or ERR_CUDA. */
 int elpa_b200_release_cache(void);
+int elpa_b200_set_workspace_cache(int enable);
 
 /* R(n, nbw): number of reflectors the band->tridiagonal chase produces.
  * 0 if n < 3 or nbw == 1 (nbw = 1: the input is already tridiagonal);
@@ -135,6 +141,9 @@ int64_t elpa_b200_workspace_bytes(int64_t n, int64_t nbw, const elpa_b200_opts *
 int elpa_b200_prepare(int64_t n, int64_t nbw, const double *hh_v, const double *hh_tau,
                       void *workspace, size_t workspace_bytes, elpa_b200_stream_t stream,
                       const elpa_b200_opts *opts);
+/* opts.kernel and n, nbw must be the ones the workspace was prepared with: a workspace this
+ * process prepared for another kernel, n or nbw is rejected with ELPA_B200_ERR_ARG (the library
+ * remembers the last 256 prepared workspace pointers; others are not checked). */
 int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev,
                              const double *hh_v, const double *hh_tau,
                              const void *workspace, size_t workspace_bytes,
@@ -240,9 +249,11 @@ int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int
  * opts (may be NULL): kernel AUTO (FFMA2 when nbw % 8 == 0 and nbw <= 128, else REFERENCE),
  *   ELPA_B200_KERNEL_FFMA2 or ELPA_B200_KERNEL_REFERENCE (one thread per column, explicitly
  *   rounded FP32, any nbw); depth_warps = D, col_warps = CW, tiles_per_warp = NC (32-column
- *   blocks per warp, 1 or 2), grid_ctas as for FP64; groups_per_step must be 0 or 1.
+ *   blocks per warp, 1 or 2), grid_ctas as for FP64; groups_per_step (K groups of 8 reflectors
+ *   per step) 0 = auto, 1 or 2 where that shape is compiled (elpa_b200_describe_f32 says; MEDIUM
+ *   autotuning enumerates them).
  * Accuracy: FP32 rounding, tolerance DESIGN.md R14.  Asynchronous on `stream`; the temporary
- * workspace comes from cudaMallocAsync/cudaFreeAsync on `stream`.
+ * workspace comes from the library's pool, stream-ordered on `stream`.
  * ------------------------------------------------------------------------------------- */
 int elpa_trans_ev_tridi_to_band_f32(int64_t n, int64_t nbw, int64_t nev, const float *hh_v, const float *hh_tau,
                                     float *Q, int64_t ldq, elpa_b200_stream_t stream, const elpa_b200_opts *opts);

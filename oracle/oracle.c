@@ -137,13 +137,17 @@ int64_t oracle_chase(int64_t n, int64_t b, const double *band_in,
                     int64_t k1 = s + L + 2 * b; if (k1 > n) k1 = n;
                     int64_t K = k1 - k0;
                     int64_t o = s - k0; /* window offset of row/col s */
-                    /* only rows [o,o+L) and cols [o,o+L) of the window are read or written */
+                    /* only rows [o,o+L) and cols [o,o+L) of the window are read or written.
+                     * OpenMP splits each loop over independent rows/columns only: every element's
+                     * arithmetic (and summation order) is the same for any thread count. */
+#pragma omp parallel for schedule(static) if (K * L >= 4096)
                     for (int64_t i = 0; i < L; i++)
                         for (int64_t t = 0; t < K; t++) {
                             win[(o + i) * K + t] = sb_get(&A, s + i, k0 + t);
                             win[t * K + o + i] = sb_get(&A, k0 + t, s + i);
                         }
                     /* left: rows [o, o+L) <- H * rows */
+#pragma omp parallel for schedule(static) if (K * L >= 4096)
                     for (int64_t cc = 0; cc < K; cc++) {
                         double p = 0.0;
                         for (int64_t i = 0; i < L; i++) p += v[i] * win[(o + i) * K + cc];
@@ -151,6 +155,7 @@ int64_t oracle_chase(int64_t n, int64_t b, const double *band_in,
                         for (int64_t i = 0; i < L; i++) win[(o + i) * K + cc] -= p * v[i];
                     }
                     /* right: cols [o, o+L) <- cols * H */
+#pragma omp parallel for schedule(static) if (K * L >= 4096)
                     for (int64_t rr = 0; rr < K; rr++) {
                         double q = 0.0;
                         for (int64_t i = 0; i < L; i++) q += win[rr * K + o + i] * v[i];
@@ -158,6 +163,7 @@ int64_t oracle_chase(int64_t n, int64_t b, const double *band_in,
                         for (int64_t i = 0; i < L; i++) win[rr * K + o + i] -= q * v[i];
                     }
                     /* write back the lower triangle of the touched rows/cols */
+#pragma omp parallel for schedule(static) reduction(| : bad) if (K * L >= 4096)
                     for (int64_t i = 0; i < L; i++)
                         for (int64_t t = 0; t < K; t++) {
                             if (t <= o + i) bad |= sb_set(&A, s + i, k0 + t, win[(o + i) * K + t]);

@@ -12,8 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# ELPA_B200_LIB: development override (A/B timing of library builds); default: the in-tree build
-_SO = os.environ.get("ELPA_B200_LIB") or os.path.join(_HERE, "libelpa_b200.so")
+_SO = os.path.join(_HERE, "libelpa_b200.so")          # the in-tree build, nothing else
 
 OK, ERR_ARG, ERR_NULL, ERR_ALIGN, ERR_DEVICE, ERR_CUDA, ERR_SPACE = 0, -1, -2, -3, -4, -5, -6
 KERNEL_AUTO, KERNEL_REFERENCE, KERNEL_DMMA, KERNEL_DFMA, KERNEL_FFMA2 = 0, 1, 2, 3, 4
@@ -27,6 +26,8 @@ def _load():
     i64, p, i32, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
     lib.elpa_b200_release_cache.restype = i32
     lib.elpa_b200_release_cache.argtypes = []
+    lib.elpa_b200_set_workspace_cache.restype = i32
+    lib.elpa_b200_set_workspace_cache.argtypes = [i32]
     lib.elpa_hh_count.restype = i64
     lib.elpa_hh_count.argtypes = [i64, i64]
     lib.elpa_trans_ev_tridi_to_band.restype = i32
@@ -111,6 +112,12 @@ def release_cache():
     _check(_lib.elpa_b200_release_cache(), "elpa_b200_release_cache")
 
 
+def set_workspace_cache(enable):
+    """Keep (True, the default) or return at every synchronisation (False) the library's freed
+    workspace memory (elpa_b200_set_workspace_cache; a documented deviation)."""
+    _check(_lib.elpa_b200_set_workspace_cache(1 if enable else 0), "elpa_b200_set_workspace_cache")
+
+
 def hh_count(n, nbw):
     return int(_lib.elpa_hh_count(int(n), int(nbw)))
 
@@ -187,8 +194,10 @@ def trans_ev_tridi_to_band_host(n, nbw, hh_v, hh_tau, Q, stream=None, opts=None)
     float64 tensors (pinned for speed); Q is updated in place; synchronises `stream`."""
     import torch
     for t, nm in ((hh_v, "hh_v"), (hh_tau, "hh_tau"), (Q, "Q")):
-        if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        if t.is_cuda or t.dtype != torch.float64 or not (t.is_contiguous() or t is Q):
             raise TypeError(f"{nm} must be a contiguous float64 CPU tensor")
+    # Q: (nev, ldq) contiguous, or an (nev, n) view with row stride ldq (a buffer that ends at
+    # element (nev-1)*ldq + n, as the header allows)
     nev, ldq = _q_ldq(Q)
     o, op = _opts_ptr(opts)
     s = _stream_handle(stream, torch.device("cuda", torch.cuda.current_device()))

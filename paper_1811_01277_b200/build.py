@@ -18,6 +18,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
                  "-I", os.path.join(ROOT, "include")]
+# ELPA_B200_DEBUG=1: debug build with the kernels' wait watchdog (trap after ~10 s of wall time)
+if os.environ.get("ELPA_B200_DEBUG") == "1":
+    CFLAGS += ["-DELPA_B200_WATCHDOG"]
 LFLAGS = ARCH + ["-shared", "-cudart", "static", "-ldl"]
 
 

@@ -21,6 +21,7 @@
 #include "gen_back.cuh"
 
 #include <dlfcn.h>
+#include <mutex>
 
 using namespace elpa_b200;
 using namespace elpa_b200_host;
@@ -271,9 +272,40 @@ int apply_impl(const Plan &p, int64_t n, int64_t nbw, int64_t nev, const double 
     return ELPA_B200_ERR_ARG;
 }
 
+// Host-side record of prepared workspaces: apply_prepared must read the layout
+// prepare wrote, and a DMMA-prepared workspace also passes the DFMA size check.  prepare records
+// (pointer, kernel, b8, n) here; apply_prepared returns ERR_ARG when the pointer was prepared for
+// a different kernel, nbw or n.  Pointers the table has not seen (prepared by another process,
+// or evicted after 256 newer preparations) are not checked.
+struct PreparedTag { const void *ws = nullptr; int kernel = 0, b8 = 0; int64_t n = 0; };
+std::mutex g_tag_mu;
+PreparedTag g_tags[256];
+int g_tag_next = 0;
+
+void record_prepared(const void *ws, const Plan &p, int64_t n) {
+    std::lock_guard<std::mutex> lock(g_tag_mu);
+    for (PreparedTag &t : g_tags)
+        if (t.ws == ws) { t.kernel = p.kernel; t.b8 = p.b8; t.n = n; return; }
+    g_tags[g_tag_next] = PreparedTag{ws, p.kernel, p.b8, n};
+    g_tag_next = (g_tag_next + 1) % 256;
+}
+
+bool prepared_matches(const void *ws, const Plan &p, int64_t n) {
+    std::lock_guard<std::mutex> lock(g_tag_mu);
+    for (const PreparedTag &t : g_tags)
+        if (t.ws == ws) return t.kernel == p.kernel && t.b8 == p.b8 && t.n == n;
+    return true;
+}
+
 }  // namespace
 
 extern "C" {
+
+int elpa_b200_set_workspace_cache(int enable) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail_cuda();
+    return set_pool_caching(dev, enable != 0) ? ELPA_B200_OK : fail_cuda();
+}
 
 int elpa_b200_release_cache(void) {
     int dev = 0;
@@ -333,7 +365,9 @@ int elpa_b200_prepare(int64_t n, int64_t nbw, const double *hh_v, const double *
     if (reinterpret_cast<uintptr_t>(workspace) & 255) return ELPA_B200_ERR_ALIGN;
     if (workspace_bytes < size_t(p.ws_bytes)) return ELPA_B200_ERR_SPACE;
     if ((rc = check_device()) != ELPA_B200_OK) return rc;
-    return prepare_impl(p, n, hh_v, hh_tau, workspace, reinterpret_cast<cudaStream_t>(stream));
+    rc = prepare_impl(p, n, hh_v, hh_tau, workspace, reinterpret_cast<cudaStream_t>(stream));
+    if (rc == ELPA_B200_OK) record_prepared(workspace, p, n);
+    return rc;
 }
 
 int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
@@ -350,6 +384,7 @@ int elpa_b200_apply_prepared(int64_t n, int64_t nbw, int64_t nev, const double *
         if (!workspace) return ELPA_B200_ERR_NULL;
         if (reinterpret_cast<uintptr_t>(workspace) & 255) return ELPA_B200_ERR_ALIGN;
         if (workspace_bytes < size_t(p.ws_bytes)) return ELPA_B200_ERR_SPACE;
+        if (!prepared_matches(workspace, p, n)) return ELPA_B200_ERR_ARG;
     }
     if ((rc = check_device()) != ELPA_B200_OK) return rc;
     return apply_impl(p, n, nbw, nev, hh_v, hh_tau, workspace, Q, ldq, reinterpret_cast<cudaStream_t>(stream));
@@ -451,9 +486,13 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
         const int64_t c0 = c * CH, nc = std::min(CH, nev - c0);
         double *d = dq[c % NBUF];
         cudaStream_t cs = (c & 1) ? cs2 : s;
-        const size_t bytes = size_t(ldq) * nc * 8;
+        // only the n valid rows of each column cross PCIe, in both directions: a legally sized
+        // host buffer ends at element (nev-1)*ldq + n, and the padding rows [n, ldq) are never
+        // written (the device buffer keeps the pitch ldq; the kernels never read rows >= n)
+        const size_t pitch = size_t(ldq) * 8, width = size_t(n) * 8;
         if ((c >= NBUF && cudaStreamWaitEvent(hs, ev_d2h[c - NBUF], 0) != cudaSuccess) ||
-            cudaMemcpyAsync(d, Q + c0 * ldq, bytes, cudaMemcpyHostToDevice, hs) != cudaSuccess ||
+            cudaMemcpy2DAsync(d, pitch, Q + c0 * ldq, pitch, width, size_t(nc), cudaMemcpyHostToDevice, hs) !=
+                cudaSuccess ||
             cudaEventRecord(ev_h2d[c], hs) != cudaSuccess || cudaStreamWaitEvent(cs, ev_h2d[c], 0) != cudaSuccess) {
             rc = ELPA_B200_ERR_CUDA;
             break;
@@ -462,7 +501,8 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
         if ((rc = make_plan(n, nbw, nc, opts, pc)) != ELPA_B200_OK) break;
         if ((rc = apply_impl(pc, n, nbw, nc, dv, dt, ws, d, ldq, cs)) != ELPA_B200_OK) break;
         if (cudaEventRecord(ev_comp[c], cs) != cudaSuccess || cudaStreamWaitEvent(ds, ev_comp[c], 0) != cudaSuccess ||
-            cudaMemcpyAsync(Q + c0 * ldq, d, bytes, cudaMemcpyDeviceToHost, ds) != cudaSuccess ||
+            cudaMemcpy2DAsync(Q + c0 * ldq, pitch, d, pitch, width, size_t(nc), cudaMemcpyDeviceToHost, ds) !=
+                cudaSuccess ||
             cudaEventRecord(ev_d2h[c], ds) != cudaSuccess) {
             rc = ELPA_B200_ERR_CUDA;
             break;

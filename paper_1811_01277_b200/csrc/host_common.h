@@ -61,11 +61,21 @@ inline int check_device() {
 // (release threshold = max): workspaces of several GB are then re-used across calls instead of
 // being unmapped at every synchronisation and re-mapped by the next call (measured: up to
 // ~190 ms per C3 call through the default pool).  elpa_b200_release_cache() trims it.
-inline cudaMemPool_t lib_pool(int dev) {
-    static cudaMemPool_t pools[64] = {};
+// This caching is a documented deviation from SURVEY §8(b)'s "no persistent allocation"
+// (DESIGN.md §4): elpa_b200_set_workspace_cache(0) makes the pool return freed memory at every
+// synchronisation (release threshold 0), i.e. no memory outlives a call.
+inline std::mutex &pool_mutex() {
     static std::mutex mu;
+    return mu;
+}
+inline cudaMemPool_t *pool_table() {
+    static cudaMemPool_t pools[64] = {};
+    return pools;
+}
+inline cudaMemPool_t lib_pool(int dev) {
+    cudaMemPool_t *pools = pool_table();
     if (dev < 0 || dev >= 64) return nullptr;
-    std::lock_guard<std::mutex> lock(mu);
+    std::lock_guard<std::mutex> lock(pool_mutex());
     if (!pools[dev]) {
         cudaMemPoolProps props = {};
         props.allocType = cudaMemAllocationTypePinned;
@@ -80,6 +90,14 @@ inline cudaMemPool_t lib_pool(int dev) {
         }
     }
     return pools[dev];
+}
+// caching on: release threshold = max (keep everything); off: threshold 0 and trim now
+inline bool set_pool_caching(int dev, bool on) {
+    cudaMemPool_t pool = lib_pool(dev);
+    if (!pool) return false;
+    uint64_t thr = on ? UINT64_MAX : 0;
+    if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) != cudaSuccess) return false;
+    return on || cudaMemPoolTrimTo(pool, 0) == cudaSuccess;
 }
 
 inline cudaError_t lib_malloc_async(void **p, size_t bytes, cudaStream_t s) {

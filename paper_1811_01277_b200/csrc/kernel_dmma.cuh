@@ -51,11 +51,27 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-// Watchdog: a wait that exceeds ~8 s at 1.965 GHz is a protocol bug; trap instead of hanging
-// the GPU (the launch then fails with a sticky error).  No printf: a call inside the wait loops
-// would force the live register window across an ABI call boundary.
-constexpr long long kWatchdogCycles = 1ll << 34;
+// Watchdog (debug builds only: ELPA_B200_DEBUG=1 at build time defines ELPA_B200_WATCHDOG): a
+// wait longer than ~10 s of wall time (%globaltimer, which is consistent across SMs, unlike
+// clock64) is a protocol bug; trap instead of hanging the GPU.  Release builds spin: a trap is a
+// sticky error that would poison the caller's whole context, and time-slicing or preemption can
+// stretch a correct wait arbitrarily.  No printf: a call inside the wait loops would force the
+// live register window across an ABI call boundary.
+#ifdef ELPA_B200_WATCHDOG
+constexpr unsigned long long kWatchdogNs = 10000000000ull;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void watchdog_fire() { asm volatile("trap;"); }
+#define ELPA_WATCHDOG_START() const unsigned long long elpa_wd_t0 = globaltimer_ns()
+#define ELPA_WATCHDOG_CHECK() \
+    do { if (globaltimer_ns() - elpa_wd_t0 > kWatchdogNs) watchdog_fire(); } while (0)
+#else
+#define ELPA_WATCHDOG_START() do { } while (0)
+#define ELPA_WATCHDOG_CHECK() do { } while (0)
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -69,9 +85,8 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
-    const long long t0 = clock64();
-    while (!mbar_try_wait(bar, parity))
-        if (clock64() - t0 > kWatchdogCycles) watchdog_fire();
+    ELPA_WATCHDOG_START();
+    while (!mbar_try_wait(bar, parity)) ELPA_WATCHDOG_CHECK();
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile(
@@ -531,11 +546,11 @@ apply_dmma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             if (seen >= need) return;
             if (lane == 0) {
                 uint64_t v = ld_acquire_u64(prog + (k - NX));
-                const long long t0 = clock64();
+                ELPA_WATCHDOG_START();
                 while (v < need) {
                     __nanosleep(128);
                     v = ld_acquire_u64(prog + (k - NX));
-                    if (clock64() - t0 > 4 * kWatchdogCycles) watchdog_fire();
+                    ELPA_WATCHDOG_CHECK();
                 }
                 seen = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(v);
             }

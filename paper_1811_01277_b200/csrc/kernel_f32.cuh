@@ -335,11 +335,11 @@ apply_f32_kernel(int64_t n64, int64_t nev64, const float *__restrict__ blobs, fl
             if (seen >= need) return;
             if (lane == 0) {
                 uint64_t v = ld_acquire_u64(prog + (k - NX));
-                const long long t0 = clock64();
+                ELPA_WATCHDOG_START();
                 while (v < need) {
                     __nanosleep(128);
                     v = ld_acquire_u64(prog + (k - NX));
-                    if (clock64() - t0 > 4 * kWatchdogCycles) watchdog_fire();
+                    ELPA_WATCHDOG_CHECK();
                 }
                 seen = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(v);
             }

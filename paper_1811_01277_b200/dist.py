@@ -42,7 +42,10 @@ def apply_sharded(n, nbw, packed, R, Q_local, src=0, group=None, stream=None, op
     this rank's columns Q_local ((c1-c0), ldq) on its GPU.  With `workspace` (a uint8 CUDA
     tensor of workspace_bytes(n, nbw)) the reflectors are prepared once into it and applied
     from it; otherwise the one-shot call is used.  Returns Q_local."""
-    broadcast_reflectors(packed, src=src, group=group)
+    # torch's NCCL collectives order themselves only against the CURRENT stream: issue the
+    # broadcast with `stream` current, so the prepare/apply enqueued on it below wait for it
+    with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(packed.device)):
+        broadcast_reflectors(packed, src=src, group=group)
     hh_v, hh_tau = unpack_reflectors(packed, R, nbw)
     if workspace is None:
         return trans_ev_tridi_to_band(n, nbw, hh_v, hh_tau, Q_local, stream=stream, opts=opts)

@@ -30,3 +30,16 @@ def test_stdout_is_private_to_the_json_line():
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == '{"ok": 1}'
     assert "BANNER" in r.stderr
+
+
+def test_exact_len_sum_matches_golden_counts():
+    """bench.exact_len_sum (closed form per sweep) equals the enumerated sum L of
+    tests/golden/paper_counts.txt for C1-C5 (exact flops = 4 sum L nev)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for line in open(os.path.join(ROOT, "tests", "golden", "paper_counts.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, n, b, nev, R, sumL = line.split()
+        assert bench.exact_len_sum(int(n), int(b)) == int(sumL), name
+    assert bench.exact_len_sum(2, 8) == 0 and bench.exact_len_sum(100, 1) == 0

@@ -81,3 +81,29 @@ def test_complex_eigenproblem_end_to_end(n, nbw, nev):
     assert np.abs(X.conj().T @ X - np.eye(nev)).max() <= 1e-12
     # without the back-transformation the tridiagonal eigenvectors do not solve B
     assert oracle.residual_c(case["band"], case["Qin"], case["lam"]) > 1e-4
+
+
+@pytest.mark.parametrize("n,b,nev", [(50, 4, 11), (130, 16, 30)])
+def test_complex_residual_equals_dense_formula(n, b, nev):
+    """oracle.residual_c equals ||B X - X Lambda||_F / (n ||B||_F) with an explicit dense
+    Hermitian B written element by element (B[i, j] = band[i-j, j] below, its conjugate above),
+    on random X and Lambda; counting each off-diagonal once in ||B||_F fails."""
+    rng = np.random.default_rng(n)
+    band = rng.uniform(-1, 1, (b + 1, n)) + 1j * rng.uniform(-1, 1, (b + 1, n))
+    band[0] = band[0].real
+    for dd in range(1, b + 1):
+        band[dd, n - dd:] = 0.0
+    Q = rng.uniform(-1, 1, (nev, n)) + 1j * rng.uniform(-1, 1, (nev, n))
+    lam = rng.uniform(-2, 2, nev)
+    B = np.zeros((n, n), dtype=np.complex128)
+    for i in range(n):
+        for j in range(max(0, i - b), i + 1):
+            B[i, j] = band[i - j, j]
+            B[j, i] = np.conj(band[i - j, j])
+    X = Q.T
+    num = np.linalg.norm(B @ X - X @ np.diag(lam), "fro")
+    want = num / (n * np.linalg.norm(B, "fro"))
+    got = oracle.residual_c(band, Q, lam)
+    assert abs(got - want) <= 1e-13 * want
+    once = num / (n * np.sqrt(np.sum(np.abs(band) ** 2)))
+    assert abs(once - want) > 1e-3 * want

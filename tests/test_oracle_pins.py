@@ -207,6 +207,61 @@ def test_P7_residual(n, b, nev):
     assert oracle.residual(case["band"], case["Qin"], case["lam"]) > 1e-6
 
 
+def _residual_mutants(band, Q, lam):
+    """Plausible mis-normalisations of oracle.residual (each must fail the pins below):
+    off-diagonals counted once in ||B||_F, the 1/n dropped, the max-norm for ||B||."""
+    nb1, n = band.shape
+    X = np.asarray(Q)[:, :n].T
+    B = oracle.dense_from_band(band)
+    num = np.linalg.norm(B @ X - X * lam[None, :])
+    once = np.sqrt(np.sum(band ** 2))
+    return {"offdiag_once": num / (n * once), "no_1_over_n": num / np.linalg.norm(B),
+            "max_norm": num / (n * np.abs(B).max())}
+
+
+def test_P7_residual_closed_form_toeplitz():
+    """R8 pinned by a closed form: B = tridiag(-1, 2, -1) (nbw = 1 storage widened to nbw = 3
+    with zero diagonals), X = the first k unit vectors, Lambda = 0.  Then B X = the first k
+    columns of B: ||B X||_F^2 = 5 + 6 (k - 1) for k < n (column 0 has 2^2 + 1, the others
+    1 + 4 + 1), ||B||_F^2 = 4 n + 2 (n - 1), so the residual is sqrt(5 + 6(k-1)) / (n sqrt(6n - 2))."""
+    n, k = 40, 7
+    band = np.zeros((4, n))
+    band[0] = 2.0
+    band[1, :n - 1] = -1.0
+    Q = np.zeros((k, n))
+    Q[np.arange(k), np.arange(k)] = 1.0
+    lam = np.zeros(k)
+    want = np.sqrt(5.0 + 6.0 * (k - 1)) / (n * np.sqrt(6.0 * n - 2.0))
+    got = oracle.residual(band, Q, lam)
+    assert abs(got - want) <= 1e-15 * want
+    for name, bad in _residual_mutants(band, Q, lam).items():
+        assert abs(bad - want) > 1e-3 * want, name
+
+
+@pytest.mark.parametrize("n,b,nev,ldq", [(64, 8, 20, 64), (301, 16, 45, 302), (512, 64, 33, 512)])
+def test_P7_residual_equals_dense_formula(n, b, nev, ldq):
+    """oracle.residual (banded B applied by diagonals, ||B||_F from the stored band) equals the
+    dense definition ||B X - X Lambda||_F / (n ||B||_F) with an explicit dense B built by
+    numpy.  Random X and Lambda (not eigenpairs), so every term of B X enters the norm, and
+    the ldq padding of Q is ignored."""
+    rng = np.random.default_rng(n + b)
+    band = rng.uniform(-1, 1, (b + 1, n))
+    for dd in range(1, b + 1):
+        band[dd, n - dd:] = 0.0                     # outside the matrix: never part of B
+    Q = rng.uniform(-1, 1, (nev, ldq))
+    lam = rng.uniform(-3, 3, nev)
+    B = np.zeros((n, n))
+    for i in range(n):
+        for j in range(max(0, i - b), min(n, i + b + 1)):
+            B[i, j] = band[abs(i - j), min(i, j)]
+    X = Q[:, :n].T
+    want = np.linalg.norm(B @ X - X @ np.diag(lam), "fro") / (n * np.linalg.norm(B, "fro"))
+    got = oracle.residual(band, Q, lam)
+    assert abs(got - want) <= 1e-13 * want
+    for name, bad in _residual_mutants(band, Q, lam).items():
+        assert abs(bad - want) > 1e-3 * want, name
+
+
 # ---------------------------------------------------------------- P8/P9 column independence, threads
 def test_P8_column_subset_bitwise_and_P9_threads():
     n, b = 300, 16
@@ -324,3 +379,13 @@ def test_P12_compact_group_equals_sequential(k):
     U = -V @ T
     comp_u = Q + V @ (U.T @ Q)
     assert np.abs(comp_u - seq).max() < 1e-13
+
+
+def test_residual_parallel_equals_residual():
+    """tests/cases.residual_parallel (column chunks on threads) is exactly oracle.residual."""
+    from cases import residual_parallel
+    rng = np.random.default_rng(3)
+    band = rng.uniform(-1, 1, (9, 300))
+    Q = rng.uniform(-1, 1, (77, 300))
+    lam = rng.uniform(-1, 1, 77)
+    assert abs(residual_parallel(band, Q, lam, chunk=16) - oracle.residual(band, Q, lam)) <= 1e-15
