@@ -215,8 +215,12 @@ int elpa_b200_autotune_run_dtype(int64_t n, int64_t nbw, int64_t nev, int dtype,
  *          j + nbw is treated as 1.0 and rows above it are never read.
  * hh1_tau: device, K doubles (0 = identity).
  * Q      : device, n x nev column-major (ldq >= n), updated in place.
- * Blocked compact WY (panels of 128 reflectors) with FP64-tensor-core DGEMMs (cuBLAS, loaded at
- * run time: ELPA_B200_ERR_CUDA if it cannot be loaded).  Asynchronous on `stream`.
+ * Blocked compact WY (panels of 256 reflectors, B_p = I - V_p T_p V_p^T), applied last panel
+ * first as Q <- Q + U_p (V_p^T Q) with U_p = -V_p T_p; every product runs in the library's own
+ * FP64 tensor-core (DMMA) contraction kernel — no BLAS.  Asynchronous on `stream`; temporary
+ * workspace (about 2x the packed panels, n^2 doubles at nbw << n) from the library's pool.
+ * Errors: ERR_ARG (n < 0 or n > 2^31 - 64, nbw < 1, nev < 0, nev > n, ldv or ldq < max(1, n)),
+ * ERR_NULL, ERR_DEVICE, ERR_CUDA; K == 0 or nev == 0 is OK without memory access.
  * ------------------------------------------------------------------------------------- */
 int64_t elpa_b2f_count(int64_t n, int64_t nbw);   /* K, or -1 on bad arguments */
 int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double *hh1_v, int64_t ldv,
@@ -231,10 +235,10 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
  *     (diagonal included) is read; its diagonal must be nonzero (not checked).
  * Q : device, n x nev column-major (ldq >= n): in Vtilde, out V (in place).
  * Blocked left-looking triangular solve: 128 x 128 diagonal blocks inverted by an own kernel,
- * the products are DGEMMs on the FP64 tensor cores (cuBLAS, loaded at run time:
- * ELPA_B200_ERR_CUDA if it cannot be loaded).  Asynchronous on `stream`.
- * Errors: ERR_ARG (n < 0, nev < 0, nev > n, ldl or ldq < max(1, n), sizes beyond 32-bit
- * BLAS), ERR_NULL, ERR_DEVICE, ERR_CUDA; n == 0 or nev == 0 is OK without memory access.
+ * the off-diagonal updates and the inverted-block products run in the library's own FP64
+ * tensor-core (DMMA) contraction kernel — no BLAS.  Asynchronous on `stream`.
+ * Errors: ERR_ARG (n < 0 or n > 2^31 - 64, nev < 0, nev > n, ldl or ldq < max(1, n)), ERR_NULL,
+ * ERR_DEVICE, ERR_CUDA; n == 0 or nev == 0 is OK without memory access.
  * ------------------------------------------------------------------------------------- */
 int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int64_t ldl, double *Q, int64_t ldq,
                                     elpa_b200_stream_t stream);

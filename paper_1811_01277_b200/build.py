@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libelpa_b200.so")
 SOURCES = [os.path.join(CSRC, "elpa_b200.cu"), os.path.join(CSRC, "elpa_b200_f32.cu"),
-           os.path.join(CSRC, "elpa_b200_c64.cu")]
+           os.path.join(CSRC, "elpa_b200_c64.cu"), os.path.join(CSRC, "elpa_b200_dense.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
     [os.path.join(ROOT, "include", "elpa_b200.h")]
 
@@ -21,7 +21,7 @@ CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-
 # ELPA_B200_DEBUG=1: debug build with the kernels' wait watchdog (trap after ~10 s of wall time)
 if os.environ.get("ELPA_B200_DEBUG") == "1":
     CFLAGS += ["-DELPA_B200_WATCHDOG"]
-LFLAGS = ARCH + ["-shared", "-cudart", "static", "-ldl"]
+LFLAGS = ARCH + ["-shared", "-cudart", "static"]
 
 
 def stale():

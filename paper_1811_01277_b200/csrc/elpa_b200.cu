@@ -17,10 +17,7 @@
 #include "kernel_dmma.cuh"
 #include "kernel_prep.cuh"
 #include "kernel_reference.cuh"
-#include "band_to_full.cuh"
-#include "gen_back.cuh"
 
-#include <dlfcn.h>
 #include <mutex>
 
 using namespace elpa_b200;
@@ -856,178 +853,6 @@ int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh
     if (e1) cudaEventDestroy(e1);
     if (rc == ELPA_B200_OK) rc = elpa_b200_autotune_best(at, best, best_ms);
     elpa_b200_autotune_destroy(at);
-    return rc;
-}
-
-}  // extern "C"
-
-// ------------------------------------------------------------------------------------------
-// NEXT-1: band -> full back-transformation (band_to_full.cuh).  The three products per panel
-// are plain DGEMMs; cuBLAS is loaded at run time (dlopen) so the library itself has no hard
-// dependency and reuses the process's already-loaded libcublas when there is one.
-// ------------------------------------------------------------------------------------------
-namespace {
-typedef void *cublas_handle_t;
-typedef int (*cublasCreate_t)(cublas_handle_t *);
-typedef int (*cublasDestroy_t)(cublas_handle_t);
-typedef int (*cublasSetStream_t)(cublas_handle_t, cudaStream_t);
-typedef int (*cublasDgemm_t)(cublas_handle_t, int, int, int, int, int, const double *, const double *, int,
-                             const double *, int, const double *, double *, int);
-struct Cublas {
-    bool ok = false;
-    cublasCreate_t create = nullptr;
-    cublasDestroy_t destroy = nullptr;
-    cublasSetStream_t set_stream = nullptr;
-    cublasDgemm_t dgemm = nullptr;
-};
-const Cublas &cublas() {
-    static Cublas c = [] {
-        Cublas r;
-        void *h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) return r;
-        r.create = reinterpret_cast<cublasCreate_t>(dlsym(h, "cublasCreate_v2"));
-        r.destroy = reinterpret_cast<cublasDestroy_t>(dlsym(h, "cublasDestroy_v2"));
-        r.set_stream = reinterpret_cast<cublasSetStream_t>(dlsym(h, "cublasSetStream_v2"));
-        r.dgemm = reinterpret_cast<cublasDgemm_t>(dlsym(h, "cublasDgemm_v2"));
-        r.ok = r.create && r.destroy && r.set_stream && r.dgemm;
-        return r;
-    }();
-    return c;
-}
-constexpr int kOpN = 0, kOpT = 1;
-constexpr int64_t kB2FPanel = 256;
-
-// One cuBLAS handle per host thread and device, created on first use (handle creation costs
-// milliseconds; the handle carries no problem state), bound to stream s.  nullptr on failure;
-// `dev` receives the current device (handles of devices >= 64 are not cached: destroy them).
-cublas_handle_t cublas_handle(cudaStream_t s, int &dev) {
-    const Cublas &cb = cublas();
-    thread_local cublas_handle_t handles[64] = {};
-    dev = 0;
-    cudaGetDevice(&dev);
-    cublas_handle_t h = (dev >= 0 && dev < 64) ? handles[dev] : nullptr;
-    if (!h && cb.create(&h) != 0) h = nullptr;
-    if (h && dev >= 0 && dev < 64) handles[dev] = h;
-    if (h && cb.set_stream(h, s) != 0) return nullptr;
-    return h;
-}
-}  // namespace
-
-
-extern "C" {
-
-int64_t elpa_b2f_count(int64_t n, int64_t nbw) {
-    if (n < 0 || nbw < 1) return -1;
-    return n >= nbw + 2 ? n - nbw - 1 : 0;
-}
-
-int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double *hh1_v, int64_t ldv,
-                               const double *hh1_tau, double *Q, int64_t ldq, elpa_b200_stream_t stream) {
-    if (n < 0 || nbw < 1 || nev < 0 || nev > n || ldq < (n > 1 ? n : 1) || ldv < (n > 1 ? n : 1))
-        return ELPA_B200_ERR_ARG;
-    const int64_t K = elpa_b2f_count(n, nbw);
-    if (K == 0 || nev == 0) return ELPA_B200_OK;
-    if (!hh1_v || !hh1_tau || !Q) return ELPA_B200_ERR_NULL;
-    if (n > INT32_MAX || nev > INT32_MAX || ldq > INT32_MAX) return ELPA_B200_ERR_ARG;   // cuBLAS int sizes
-    int rc = check_device();
-    if (rc != ELPA_B200_OK) return rc;
-    const Cublas &cb = cublas();
-    if (!cb.ok) return ELPA_B200_ERR_CUDA;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int64_t P = kB2FPanel, np = (K + P - 1) / P;
-    const size_t bV = size_t(b2f_panel_offset(n, nbw, P, np)) * 8, bG = size_t(np) * P * P * 8;
-    const size_t bW = size_t(P) * nev * 8;
-    auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
-    char *buf = nullptr;
-    if (lib_malloc_async(reinterpret_cast<void **>(&buf), up(bV) + 2 * up(bG) + 2 * up(bW), s) != cudaSuccess)
-        return fail_cuda();
-    double *Vp = reinterpret_cast<double *>(buf), *G = reinterpret_cast<double *>(buf + up(bV));
-    double *T = reinterpret_cast<double *>(buf + up(bV) + up(bG));
-    double *W = reinterpret_cast<double *>(buf + up(bV) + 2 * up(bG)), *W2 = reinterpret_cast<double *>(
-                                                                              buf + up(bV) + 2 * up(bG) + up(bW));
-    int dev = 0;
-    cublas_handle_t h = cublas_handle(s, dev);
-    if (!h) rc = ELPA_B200_ERR_CUDA;
-    const double one = 1.0, zero = 0.0, mone = -1.0;
-    if (rc == ELPA_B200_OK) {
-        dim3 g(unsigned(std::min<int64_t>(1024, (n * P + 255) / 256)), unsigned(np));
-        b2f_build_panels<<<g, 256, 0, s>>>(n, nbw, K, P, hh1_v, ldv, Vp);
-        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
-    }
-    for (int64_t p = 0; rc == ELPA_B200_OK && p < np; p++) {   // Gram matrices G_p = V_p^T V_p
-        const int64_t m = b2f_rows(n, nbw, P, p);
-        const double *vp = Vp + b2f_panel_offset(n, nbw, P, p);
-        if (cb.dgemm(h, kOpT, kOpN, int(P), int(P), int(m), &one, vp, int(m), vp, int(m), &zero, G + p * P * P,
-                     int(P)) != 0)
-            rc = ELPA_B200_ERR_CUDA;
-    }
-    if (rc == ELPA_B200_OK) {
-        b2f_tfactor<<<unsigned(np), 256, 0, s>>>(K, P, hh1_tau, G, T);
-        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
-    }
-    for (int64_t p = np - 1; rc == ELPA_B200_OK && p >= 0; p--) {   // last panel first
-        const int64_t r0 = p * P + nbw, m = n - r0;
-        const double *vp = Vp + b2f_panel_offset(n, nbw, P, p);
-        double *q = Q + r0;
-        if (cb.dgemm(h, kOpT, kOpN, int(P), int(nev), int(m), &one, vp, int(m), q, int(ldq), &zero, W, int(P)) != 0 ||
-            cb.dgemm(h, kOpN, kOpN, int(P), int(nev), int(P), &one, T + p * P * P, int(P), W, int(P), &zero, W2,
-                     int(P)) != 0 ||
-            cb.dgemm(h, kOpN, kOpN, int(m), int(nev), int(P), &mone, vp, int(m), W2, int(P), &one, q, int(ldq)) != 0)
-            rc = ELPA_B200_ERR_CUDA;
-    }
-    if (h && !(dev >= 0 && dev < 64)) cb.destroy(h);
-    if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
-    if (rc != ELPA_B200_OK) cudaGetLastError();
-    return rc;
-}
-
-
-int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int64_t ldl, double *Q, int64_t ldq,
-                                    elpa_b200_stream_t stream) {
-    if (n < 0 || nev < 0 || nev > n || ldl < (n > 1 ? n : 1) || ldq < (n > 1 ? n : 1)) return ELPA_B200_ERR_ARG;
-    if (n == 0 || nev == 0) return ELPA_B200_OK;
-    if (!L || !Q) return ELPA_B200_ERR_NULL;
-    if (n > INT32_MAX || nev > INT32_MAX || ldq > INT32_MAX || ldl > INT32_MAX) return ELPA_B200_ERR_ARG;
-    int rc = check_device();
-    if (rc != ELPA_B200_OK) return rc;
-    const Cublas &cb = cublas();
-    if (!cb.ok) return ELPA_B200_ERR_CUDA;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    constexpr int NB = kGbBlock;
-    const int64_t nb = (n + NB - 1) / NB;
-    const size_t bInv = size_t(nb) * NB * NB * 8, bT = size_t(NB) * nev * 8;
-    char *buf = nullptr;
-    if (lib_malloc_async(reinterpret_cast<void **>(&buf), ((bInv + 255) & ~size_t(255)) + bT, s) != cudaSuccess)
-        return fail_cuda();
-    double *Linv = reinterpret_cast<double *>(buf), *T = reinterpret_cast<double *>(buf + ((bInv + 255) & ~size_t(255)));
-    int dev = 0;
-    cublas_handle_t h = cublas_handle(s, dev);
-    if (!h) rc = ELPA_B200_ERR_CUDA;
-    const size_t smem = size_t(NB) * NB * 8;
-    if (rc == ELPA_B200_OK &&
-        cudaFuncSetAttribute(gb_trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-        rc = ELPA_B200_ERR_CUDA;
-    if (rc == ELPA_B200_OK) {
-        gb_trinv_kernel<<<unsigned(nb), NB, smem, s>>>(n, L, ldl, Linv);
-        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
-    }
-    const double one = 1.0, zero = 0.0, mone = -1.0;
-    for (int64_t b = nb - 1; rc == ELPA_B200_OK && b >= 0; b--) {
-        const int64_t r0 = b * NB, m = std::min<int64_t>(NB, n - r0), r1 = r0 + m;
-        if (r1 < n && cb.dgemm(h, kOpT, kOpN, int(m), int(nev), int(n - r1), &mone, L + r0 * ldl + r1, int(ldl),
-                               Q + r1, int(ldq), &one, Q + r0, int(ldq)) != 0)
-            rc = ELPA_B200_ERR_CUDA;
-        if (rc == ELPA_B200_OK &&
-            (cb.dgemm(h, kOpT, kOpN, int(m), int(nev), int(m), &one, Linv + b * NB * NB, NB, Q + r0, int(ldq), &zero, T,
-                      NB) != 0 ||
-             cudaMemcpy2DAsync(Q + r0, size_t(ldq) * 8, T, size_t(NB) * 8, size_t(m) * 8, size_t(nev),
-                               cudaMemcpyDeviceToDevice, s) != cudaSuccess))
-            rc = ELPA_B200_ERR_CUDA;
-    }
-    if (h && !(dev >= 0 && dev < 64)) cb.destroy(h);
-    if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
-    if (rc != ELPA_B200_OK) cudaGetLastError();
     return rc;
 }
 

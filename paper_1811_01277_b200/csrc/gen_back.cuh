@@ -2,10 +2,10 @@
 //     V = (L^{-1})^T Vtilde        (Eq. 7; B = L L^T)
 // i.e. the triangular solve L^T V = Vtilde for nev columns.  Left-looking blocked form over
 // row blocks of kGbBlock from the bottom: for block b (rows [r0, r1)),
-//     Q_b <- Q_b - L[r1:n, r0:r1]^T Q[r1:n]      (DGEMM, k = n - r1)
-//     Q_b <- (L_bb^{-1})^T Q_b                    (DGEMM with the inverted diagonal block)
-// This file holds the diagonal-block inversion kernel; the products are plain DGEMMs on the
-// FP64 tensor cores (cuBLAS, loaded at run time, as for NEXT-1).
+//     Q_b <- Q_b - L[r1:n, r0:r1]^T Q[r1:n]      (contraction, k = n - r1)
+//     Q_b <- (L_bb^{-1})^T Q_b                    (contraction with the inverted diagonal block)
+// This file holds the diagonal-block inversion kernel; the products run in the library's own
+// DMMA contraction (dgemm_dmma.cuh), as for NEXT-1.
 #pragma once
 #include <stdint.h>
 
