@@ -74,25 +74,88 @@ b2f_transpose_panel(int64_t m, int64_t ld, int64_t P, const double *__restrict__
     }
 }
 
-// T factor of every panel from its Gram matrix G_p = V_p^T V_p (P x P, symmetric):
-// T[a][a] = tau_a, T[0:a, a] = -tau_a T[0:a, 0:a] G[0:a, a]  (LAPACK dlarft, forward), T stored
-// column-major (T[a*P + i] = T[i][a]).  One CTA per panel; the column recurrence is sequential.
-__global__ void __launch_bounds__(256)
+// T factor of every panel from its Gram matrix G_p = V_p^T V_p (P x P, symmetric), LAPACK dlarft
+// forward: T[a][a] = tau_a, T[0:a, a] = -tau_a T[0:a, 0:a] G[0:a, a].  T is stored column-major
+// (T[a*P + i] = T[i][a]).  Blocked in 64 x 64 blocks (the recurrence for a block column of
+// reflectors J given the earlier ones is T[0:J, J] = -T[0:J, 0:J] G[0:J, J] T_JJ, the standard
+// two-block form of the compact WY factor):
+//   1. T_JJ by the column recurrence above on the diagonal block, in shared memory;
+//   2. for every earlier row block I: X = sum_{K = I}^{J-1} T[I, K] G[K, J]  (T is upper
+//      triangular), then T[I, J] = -X T_JJ, block products from shared memory.
+// One CTA (512 threads) per panel; P must be a multiple of 64.  (The unblocked recurrence read
+// T from L2 one dependent load at a time: 14 ms per call at n = 20000, P = 512.)
+constexpr int kTB = 64, kTS = 65;                 // block size, padded shared-memory row stride
+constexpr size_t kTfactorSmem = size_t(4) * kTB * kTS * sizeof(double);
+
+__global__ void __launch_bounds__(512)
 b2f_tfactor(int64_t K, int64_t P, const double *__restrict__ tau, const double *__restrict__ G,
             double *__restrict__ T) {
+    extern __shared__ double sm[];
+    double *Gd = sm, *Td = sm + kTB * kTS, *Ab = sm + 2 * kTB * kTS, *Bb = sm + 3 * kTB * kTS;
     const int64_t p = blockIdx.x;
     const double *g = G + p * P * P;
     double *t = T + p * P * P;
-    for (int64_t e = threadIdx.x; e < P * P; e += blockDim.x) t[e] = 0.0;
-    __syncthreads();
-    for (int64_t a = 0; a < P; a++) {
-        const double ta = (p * P + a < K) ? tau[p * P + a] : 0.0;
-        for (int64_t i = threadIdx.x; i < a; i += blockDim.x) {
-            double acc = 0.0;
-            for (int64_t k = i; k < a; k++) acc = fma(t[k * P + i], g[a * P + k], acc);
-            t[a * P + i] = -ta * acc;      // reads column a-1 and earlier only
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int r = tid >> 3, c0 = (tid & 7) * 8;     // block products: row r, columns c0 .. c0+7
+    const int nb = int(P / kTB);
+    for (int64_t e = tid; e < P * P; e += nt) t[e] = 0.0;
+    for (int J = 0; J < nb; J++) {
+        const int64_t a0 = int64_t(J) * kTB;
+        // 1. diagonal block
+        for (int e = tid; e < kTB * kTB; e += nt) {
+            const int i = e % kTB, k = e / kTB;         // G column-major: G[k][i] at g[k*P + i]
+            Gd[i * kTS + k] = g[(a0 + k) * P + a0 + i];
+            Td[i * kTS + k] = 0.0;
         }
-        if (threadIdx.x == 0) t[a * P + a] = ta;
+        __syncthreads();
+        for (int a = 0; a < kTB; a++) {
+            const double ta = (p * P + a0 + a < K) ? tau[p * P + a0 + a] : 0.0;
+            if (tid < a) {
+                double s = 0.0;
+                for (int k = tid; k < a; k++) s = fma(Td[tid * kTS + k], Gd[k * kTS + a], s);
+                Td[tid * kTS + a] = -ta * s;
+            }
+            if (tid == a) Td[a * kTS + a] = ta;
+            __syncthreads();
+        }
+        for (int e = tid; e < kTB * kTB; e += nt) {
+            const int i = e % kTB, k = e / kTB;
+            t[(a0 + k) * P + a0 + i] = Td[i * kTS + k];
+        }
+        // 2. off-diagonal blocks T[I, J], I < J
+        for (int I = 0; I < J; I++) {
+            double acc[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) acc[u] = 0.0;
+            for (int Kb = I; Kb < J; Kb++) {
+                __syncthreads();
+                for (int e = tid; e < kTB * kTB; e += nt) {
+                    const int i = e % kTB, k = e / kTB;
+                    Ab[i * kTS + k] = __ldcg(t + (int64_t(Kb) * kTB + k) * P + int64_t(I) * kTB + i);   // T[I,Kb]
+                    Bb[i * kTS + k] = g[(a0 + k) * P + int64_t(Kb) * kTB + i];                           // G[Kb,J]
+                }
+                __syncthreads();
+                for (int k = 0; k < kTB; k++) {
+                    const double av = Ab[r * kTS + k];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) acc[u] = fma(av, Bb[k * kTS + c0 + u], acc[u]);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 8; u++) Ab[r * kTS + c0 + u] = acc[u];      // X
+            __syncthreads();
+            double out[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) out[u] = 0.0;
+            for (int k = 0; k < kTB; k++) {
+                const double xv = Ab[r * kTS + k];
+#pragma unroll
+                for (int u = 0; u < 8; u++) out[u] = fma(xv, Td[k * kTS + c0 + u], out[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) t[(a0 + c0 + u) * P + int64_t(I) * kTB + r] = -out[u];
+        }
         __syncthreads();
     }
 }

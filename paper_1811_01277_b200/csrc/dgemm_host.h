@@ -1,0 +1,78 @@
+// dgemm_host.h — launch logic of the library's DMMA contraction (dgemm_dmma.cuh): the split-K
+// choice and the scratch it needs.  Used by elpa_b200_dense.cu (NEXT-1, NEXT-4).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "dgemm_dmma.cuh"
+#include "host_common.h"
+
+namespace elpa_b200_host {
+
+using GemmCfg = elpa_b200::gemm::Main;
+
+// Split count for C = A^T B with an M x N output and reduction length K.  A small output (the
+// V^T Q and L^T Q products have N = 128..256) has a few waves of tiles or fewer, so K is split
+// into S slices; S minimises (waves) x (k-steps per slice) plus the partial-sum traffic, in
+// seconds at the kernel's per-CTA rate.
+inline int gemm_split(int64_t M, int64_t N, int64_t K) {
+    using elpa_b200::gemm::BK;
+    const int64_t tiles = ((M + GemmCfg::BM - 1) / GemmCfg::BM) * ((N + GemmCfg::BN - 1) / GemmCfg::BN);
+    const int64_t slots = int64_t(GemmCfg::MINB) * sm_count();           // resident CTAs
+    const int64_t ksteps = (K + BK - 1) / BK;
+    const double step_s = 2.0 * GemmCfg::BM * GemmCfg::BN * BK / (36.9e12 / double(slots));
+    double best = 1e300;
+    int bs = 1;
+    for (int S = 1; S <= 16; S++) {
+        const int64_t per = (ksteps + S - 1) / S;
+        if (S > 1 && per < 8) break;
+        const int64_t waves = (tiles * S + slots - 1) / slots;
+        const double t = double(waves) * double(per) * step_s + (S > 1 ? double(S + 1) * M * N * 8 / 6e12 : 0.0);
+        if (t < best * 0.97) { best = t; bs = S; }
+    }
+    return bs;
+}
+
+inline int64_t gemm_tiles(int64_t M, int64_t N) {
+    return ((M + GemmCfg::BM - 1) / GemmCfg::BM) * ((N + GemmCfg::BN - 1) / GemmCfg::BN);
+}
+
+// doubles of split-K scratch one call needs (0 without a split)
+inline int64_t gemm_scratch_doubles(int64_t M, int64_t N, int64_t K) {
+    const int S = gemm_split(M, N, K);
+    return S > 1 ? int64_t(S) * gemm_tiles(M, N) * GemmCfg::BM * GemmCfg::BN : 0;
+}
+
+// C (row-major, ldc) = alpha * A^T B (+ beta * C): A (K x M), B (K x N) column-major.
+// `scratch` holds gemm_scratch_doubles(M, N, K) doubles; `counters` gemm_tiles(M, N) unsigned
+// zero-initialised words (they are left zero again).  alpha must be nonzero.
+inline int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
+                   int64_t ldb, double beta, double *C, int64_t ldc, double *scratch, unsigned *counters,
+                   cudaStream_t s) {
+    using namespace elpa_b200::gemm;
+    if (M <= 0 || N <= 0) return ELPA_B200_OK;
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || alpha == 0.0) return ELPA_B200_ERR_ARG;
+    static bool attr = [] {
+        cudaFuncSetAttribute(dgemm_tn_kernel<GemmCfg, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(GemmCfg::SMEM));
+        cudaFuncSetAttribute(dgemm_tn_kernel<GemmCfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(GemmCfg::SMEM));
+        return cudaGetLastError() == cudaSuccess;
+    }();
+    if (!attr) return ELPA_B200_ERR_CUDA;
+    const int S = K > 0 ? gemm_split(M, N, K) : 1;
+    const int64_t kps = K > 0 ? ((K + S - 1) / S + BK - 1) / BK * BK : 0;
+    const int tx = int((N + GemmCfg::BN - 1) / GemmCfg::BN), ty = int((M + GemmCfg::BM - 1) / GemmCfg::BM);
+    const dim3 grid{unsigned(tx), unsigned(ty), unsigned(S)};
+    if (beta != 0.0)
+        dgemm_tn_kernel<GemmCfg, true><<<grid, GemmCfg::THREADS, GemmCfg::SMEM, s>>>(
+            int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb, beta, C, ldc, scratch, counters);
+    else
+        dgemm_tn_kernel<GemmCfg, false><<<grid, GemmCfg::THREADS, GemmCfg::SMEM, s>>>(
+            int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb, 0.0, C, ldc, scratch, counters);
+    return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+}
+
+}  // namespace elpa_b200_host

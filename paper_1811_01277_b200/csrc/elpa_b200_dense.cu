@@ -9,7 +9,7 @@
 
 #include "../../include/elpa_b200.h"
 #include "host_common.h"
-#include "dgemm_dmma.cuh"
+#include "dgemm_host.h"
 #include "band_to_full.cuh"
 #include "gen_back.cuh"
 
@@ -18,67 +18,10 @@ using namespace elpa_b200_host;
 
 namespace {
 
-constexpr int64_t kB2FPanel = 256;
-
-// Split count for C = A^T B with an M x N output and reduction length K: the tile count of a
-// small output (the V^T Q and L^T Q products have N = 128..256) is a few waves of one CTA per SM
-// or less, so K is split into S slices; S minimises (waves) x (K per slice) plus the cost of the
-// extra partial-sum traffic, in units of one 16-deep k-step of a tile.
-int choose_split(int64_t M, int64_t N, int64_t K) {
-    using namespace gemm;
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    const int64_t slots = sm_count();
-    const int64_t ksteps = (K + BK - 1) / BK;
-    double best = 1e300;
-    int bs = 1;
-    for (int S = 1; S <= 16; S++) {
-        const int64_t per = (ksteps + S - 1) / S;
-        if (S > 1 && per < 8) break;
-        const int64_t waves = (tiles * S + slots - 1) / slots;
-        // one k-step of a tile ~ 2*128*128*16 flops at ~0.25 TF/s per SM = 2.1 us; the partial
-        // sums cost (S + 1) * M * N * 8 bytes at ~5 TB/s
-        const double t = double(waves) * double(per) * 2.1e-6 + (S > 1 ? double(S + 1) * M * N * 8 / 5e12 : 0.0);
-        if (t < best * 0.98) { best = t; bs = S; }
-    }
-    return bs;
-}
-
-// C (row-major, ldc) = alpha * A^T B (+ beta * C): A (K x M), B (K x N) column-major.  `scratch`
-// (>= gemm_scratch_doubles(M, N, K) doubles) holds the split-K partials.
-int64_t gemm_scratch_doubles(int64_t M, int64_t N, int64_t K) {
-    const int S = choose_split(M, N, K);
-    return S > 1 ? int64_t(S) * M * N : 0;
-}
-
-int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B, int64_t ldb,
-            double beta, double *C, int64_t ldc, double *scratch, cudaStream_t s) {
-    using namespace gemm;
-    if (M <= 0 || N <= 0) return ELPA_B200_OK;
-    static bool attr = [] {
-        cudaFuncSetAttribute(dgemm_tn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
-        cudaFuncSetAttribute(dgemm_tn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
-        return cudaGetLastError() == cudaSuccess;
-    }();
-    if (!attr) return ELPA_B200_ERR_CUDA;
-    const int S = K > 0 ? choose_split(M, N, K) : 1;
-    const int64_t kps = K > 0 ? ((K + S - 1) / S + BK - 1) / BK * BK : 0;
-    dim3 grid(unsigned((N + BN - 1) / BN), unsigned((M + BM - 1) / BM), unsigned(S));
-    if (S == 1) {
-        if (beta != 0.0)
-            dgemm_tn_kernel<true><<<grid, THREADS, SMEM, s>>>(int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb,
-                                                            beta, C, ldc, 0);
-        else
-            dgemm_tn_kernel<false><<<grid, THREADS, SMEM, s>>>(int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb,
-                                                             0.0, C, ldc, 0);
-    } else {
-        dgemm_tn_kernel<false><<<grid, THREADS, SMEM, s>>>(int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb, 0.0,
-                                                         scratch, N, M * N);
-        const int64_t total = M * N;
-        const unsigned rb = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16));
-        splitk_reduce_kernel<<<rb, 256, 0, s>>>(int(M), int(N), S, scratch, N, M * N, beta, nullptr, 0, C, ldc);
-    }
-    return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
-}
+// Panel width: the Q update's reduction length.  512 measured 0.88 of the DMMA peak for the update
+// and 0.91 for V^T Q against 0.84 / 0.89 at 256 (tools/gemm_bench.cu); the G and U products it adds
+// cost 2.6% of the flops.
+constexpr int64_t kB2FPanel = 512;
 
 size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -106,26 +49,29 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
     // workspace: V panels and U^T panels (same size), G and T per panel, one panel's V^T, W^T,
     // and the split-K partials of the largest product of each kind
     const size_t nV = size_t(b2f_panel_offset(n, nbw, P, np));
-    size_t nScr = 0;
+    size_t nScr = 0, nCnt = 0;
     for (int64_t p = 0; p < np; p++) {
         const int64_t m = b2f_rows(n, nbw, P, p);
+        nCnt = std::max<size_t>({nCnt, size_t(gemm_tiles(m, P)), size_t(gemm_tiles(nev, P)), size_t(gemm_tiles(nev, m))});
         nScr = std::max<size_t>(nScr, size_t(gemm_scratch_doubles(P, P, m)));        // G
         nScr = std::max<size_t>(nScr, size_t(gemm_scratch_doubles(m, P, P)));        // U^T
         nScr = std::max<size_t>(nScr, size_t(gemm_scratch_doubles(nev, P, m)));      // W^T
         nScr = std::max<size_t>(nScr, size_t(gemm_scratch_doubles(nev, m, P)));      // Q update
     }
     const size_t bV = up256(nV * 8), bG = up256(size_t(np) * P * P * 8), bVT = up256(size_t(ld0) * P * 8);
-    const size_t bW = up256(size_t(nev) * P * 8), bS = up256(nScr * 8);
+    const size_t bW = up256(size_t(nev) * P * 8), bS = up256(nScr * 8), bC = up256(nCnt * 4);
     char *buf = nullptr;
-    if (lib_malloc_async(reinterpret_cast<void **>(&buf), 2 * bV + 2 * bG + bVT + bW + bS, s) != cudaSuccess)
+    if (lib_malloc_async(reinterpret_cast<void **>(&buf), 2 * bV + 2 * bG + bVT + bW + bS + bC, s) != cudaSuccess)
         return fail_cuda();
+    unsigned *cnt = reinterpret_cast<unsigned *>(buf + 2 * bV + 2 * bG + bVT + bW + bS);
+    if (cudaMemsetAsync(cnt, 0, nCnt * 4, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     double *Vp = reinterpret_cast<double *>(buf), *UT = reinterpret_cast<double *>(buf + bV);
     double *G = reinterpret_cast<double *>(buf + 2 * bV), *T = reinterpret_cast<double *>(buf + 2 * bV + bG);
     double *VT = reinterpret_cast<double *>(buf + 2 * bV + 2 * bG);
     double *Wt = reinterpret_cast<double *>(buf + 2 * bV + 2 * bG + bVT);
     double *scr = reinterpret_cast<double *>(buf + 2 * bV + 2 * bG + bVT + bW);
     (void)m0;
-    {
+    if (rc == ELPA_B200_OK) {
         dim3 g(unsigned(std::min<int64_t>(1024, (ld0 * P + 255) / 256)), unsigned(np));
         b2f_build_panels<<<g, 256, 0, s>>>(n, nbw, K, P, hh1_v, ldv, Vp);
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
@@ -134,10 +80,13 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
     for (int64_t p = 0; rc == ELPA_B200_OK && p < np; p++) {
         const int64_t ld = b2f_ld(n, nbw, P, p);
         const double *vp = Vp + b2f_panel_offset(n, nbw, P, p);
-        rc = gemm_tn(P, P, ld, 1.0, vp, ld, vp, ld, 0.0, G + p * P * P, P, scr, s);
+        rc = gemm_tn(P, P, ld, 1.0, vp, ld, vp, ld, 0.0, G + p * P * P, P, scr, cnt, s);
     }
     if (rc == ELPA_B200_OK) {
-        b2f_tfactor<<<unsigned(np), 256, 0, s>>>(K, P, hh1_tau, G, T);
+        static bool attr = cudaFuncSetAttribute(b2f_tfactor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(kTfactorSmem)) == cudaSuccess;
+        if (!attr) rc = ELPA_B200_ERR_CUDA;
+        else b2f_tfactor<<<unsigned(np), 512, kTfactorSmem, s>>>(K, P, hh1_tau, G, T);
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     }
     for (int64_t p = 0; rc == ELPA_B200_OK && p < np; p++) {
@@ -146,14 +95,14 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
         b2f_transpose_panel<<<g, 256, 0, s>>>(ld, ld, P, Vp + off, VT);
         if (cudaGetLastError() != cudaSuccess) { rc = ELPA_B200_ERR_CUDA; break; }
         // UT[i*P + c] = -sum_a V[i][a] T[a][c]:  A = V^T (K = a, M = i), B = T (K = a, N = c)
-        rc = gemm_tn(ld, P, P, -1.0, VT, P, T + p * P * P, P, 0.0, UT + off, P, scr, s);
+        rc = gemm_tn(ld, P, P, -1.0, VT, P, T + p * P * P, P, 0.0, UT + off, P, scr, cnt, s);
     }
     // apply, last panel first:  W^T = Q^T V_p,  Q^T += W^T U_p^T  (rows r0' .. n of Q)
     for (int64_t p = np - 1; rc == ELPA_B200_OK && p >= 0; p--) {
         const int64_t r0 = b2f_origin(nbw, P, p), m = n - r0, ld = b2f_ld(n, nbw, P, p);
         const int64_t off = b2f_panel_offset(n, nbw, P, p);
-        rc = gemm_tn(nev, P, m, 1.0, Q + r0, ldq, Vp + off, ld, 0.0, Wt, P, scr, s);
-        if (rc == ELPA_B200_OK) rc = gemm_tn(nev, m, P, 1.0, Wt, P, UT + off, P, 1.0, Q + r0, ldq, scr, s);
+        rc = gemm_tn(nev, P, m, 1.0, Q + r0, ldq, Vp + off, ld, 0.0, Wt, P, scr, cnt, s);
+        if (rc == ELPA_B200_OK) rc = gemm_tn(nev, m, P, 1.0, Wt, P, UT + off, P, 1.0, Q + r0, ldq, scr, cnt, s);
     }
     if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
     if (rc != ELPA_B200_OK) cudaGetLastError();
@@ -172,6 +121,7 @@ int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int
     constexpr int NB = kGbBlock;
     const int64_t nb = (n + NB - 1) / NB;
     size_t nScr = 0;
+    const size_t nCnt = size_t(gemm_tiles(nev, NB));
     for (int64_t b = 0; b < nb; b++) {
         const int64_t r1 = std::min<int64_t>(n, (b + 1) * NB);
         nScr = std::max<size_t>(nScr, size_t(gemm_scratch_doubles(nev, NB, n - r1)));
@@ -179,11 +129,15 @@ int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int
     }
     const size_t bInv = up256(size_t(nb) * NB * NB * 8), bT = up256(size_t(NB) * nev * 8), bS = up256(nScr * 8);
     char *buf = nullptr;
-    if (lib_malloc_async(reinterpret_cast<void **>(&buf), bInv + bT + bS, s) != cudaSuccess) return fail_cuda();
+    if (lib_malloc_async(reinterpret_cast<void **>(&buf), bInv + bT + bS + up256(nCnt * 4), s) != cudaSuccess)
+        return fail_cuda();
+    unsigned *cnt = reinterpret_cast<unsigned *>(buf + bInv + bT + bS);
+    if (cudaMemsetAsync(cnt, 0, nCnt * 4, s) != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     double *Linv = reinterpret_cast<double *>(buf), *T = reinterpret_cast<double *>(buf + bInv);
     double *scr = reinterpret_cast<double *>(buf + bInv + bT);
     const size_t smem = size_t(NB) * NB * 8;
-    if (cudaFuncSetAttribute(gb_trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+    if (rc == ELPA_B200_OK &&
+        cudaFuncSetAttribute(gb_trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
         rc = ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
         gb_trinv_kernel<<<unsigned(nb), NB, smem, s>>>(n, L, ldl, Linv);
@@ -192,9 +146,9 @@ int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int
     // left-looking from the bottom: Q_b -= L[r1:n, r0:r1]^T Q[r1:n];  Q_b = L_bb^{-T} Q_b
     for (int64_t b = nb - 1; rc == ELPA_B200_OK && b >= 0; b--) {
         const int64_t r0 = b * NB, m = std::min<int64_t>(NB, n - r0), r1 = r0 + m;
-        if (r1 < n) rc = gemm_tn(nev, m, n - r1, -1.0, Q + r1, ldq, L + r0 * ldl + r1, ldl, 1.0, Q + r0, ldq, scr, s);
+        if (r1 < n) rc = gemm_tn(nev, m, n - r1, -1.0, Q + r1, ldq, L + r0 * ldl + r1, ldl, 1.0, Q + r0, ldq, scr, cnt, s);
         // T[c*NB + i] = sum_k Q_b[k][c] Linv[k][i]  (Linv column-major, ld NB)
-        if (rc == ELPA_B200_OK) rc = gemm_tn(nev, m, m, 1.0, Q + r0, ldq, Linv + b * NB * NB, NB, 0.0, T, NB, scr, s);
+        if (rc == ELPA_B200_OK) rc = gemm_tn(nev, m, m, 1.0, Q + r0, ldq, Linv + b * NB * NB, NB, 0.0, T, NB, scr, cnt, s);
         if (rc == ELPA_B200_OK &&
             cudaMemcpy2DAsync(Q + r0, size_t(ldq) * 8, T, size_t(NB) * 8, size_t(m) * 8, size_t(nev),
                               cudaMemcpyDeviceToDevice, s) != cudaSuccess)
