@@ -75,8 +75,10 @@ enum {
     ELPA_B200_KERNEL_DMMA = 2,      /* k = 8 compact-WY groups on FP64 tensor cores (DMMA),
                                        depth-pipelined row windows; nbw % 8 == 0, nbw <= 128
                                        (AUTO picks it then, else REFERENCE) */
-    ELPA_B200_KERNEL_DFMA = 3,      /* the same groups and schedule on FP64 CUDA cores (DFMA +
-                                       warp shuffles): the measured alternative to DMMA */
+    ELPA_B200_KERNEL_DFMA = 3,      /* FP64 CUDA cores: a lane owns a column, k = fused_k
+                                       reflectors applied in sequence to a register window of
+                                       nbw + k rows (north_star item 3's design); nbw 8/16/32/64;
+                                       the measured alternative to DMMA */
     ELPA_B200_KERNEL_FFMA2 = 4      /* FP32 entry point only: packed FP32 FMA (f32x2) kernel,
                                        same schedule; nbw % 8 == 0, nbw <= 128 */
 };
@@ -90,6 +92,8 @@ typedef struct {
     int tiles_per_warp;  /* NCT: 8-column tiles per warp (1,2,4); an item has CW*NCT tiles */
     int grid_ctas;       /* persistent CTAs to launch, 0 = all co-resident (148 x occupancy) */
     int groups_per_step; /* K: reflector groups (of 8) per CTA barrier (1,2,4), 0 = auto */
+    int fused_k;         /* DFMA kernel only: reflectors fused per group, k = 2, 4, 6 or 8 (0 = 8);
+                            must be 0 for the other kernels */
 } elpa_b200_opts;
 
 /* Return the memory the library's per-device pool caches between calls (temporary workspaces)

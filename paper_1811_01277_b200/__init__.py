@@ -94,7 +94,7 @@ class Opts(ctypes.Structure):
     """elpa_b200_opts (include/elpa_b200.h)."""
     _fields_ = [("kernel", ctypes.c_int), ("depth_warps", ctypes.c_int), ("col_warps", ctypes.c_int),
                 ("tiles_per_warp", ctypes.c_int), ("grid_ctas", ctypes.c_int),
-                ("groups_per_step", ctypes.c_int)]
+                ("groups_per_step", ctypes.c_int), ("fused_k", ctypes.c_int)]
 
 
 class ElpaB200Error(RuntimeError):

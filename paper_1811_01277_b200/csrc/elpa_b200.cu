@@ -16,6 +16,7 @@
 #include "geometry.cuh"
 #include "kernel_dmma.cuh"
 #include "kernel_prep.cuh"
+#include "kernel_dfma.cuh"
 #include "kernel_reference.cuh"
 
 #include <mutex>
@@ -28,6 +29,9 @@ namespace {
 struct Plan {
     int kernel = ELPA_B200_KERNEL_REFERENCE;
     int b8 = 0, D = 1, CW = 1, NCT = 1, K = 1;
+    int64_t nbw = 0;
+    int kf = 0;                // DFMA kernel: reflectors fused per group (2, 4, 6, 8)
+    int64_t gb_off = 0;        // DFMA kernel: byte offset of the group-base table in the workspace
     int grid_req = 0;          // requested grid (0 = co-resident maximum)
     int64_t items = 0;         // (tile group, depth pass) work items
     int64_t nx = 0;            // tile groups
@@ -53,39 +57,44 @@ struct Shape { int D, CW, NCT, K; };
 #define ELPA_SHAPE_ENTRY(D_, CW_, NCT_, K_) {D_, CW_, NCT_, K_},
 constexpr Shape kShapes[] = {ELPA_SHAPES(ELPA_SHAPE_ENTRY)};
 
-// the DFMA comparison kernel is compiled for a smaller menu
-#define ELPA_DFMA_SHAPES(X) X(1, 2, 2, 1) X(2, 2, 2, 1) X(1, 4, 2, 1) X(2, 4, 2, 1) X(1, 2, 4, 1) X(2, 2, 4, 1)
-constexpr Shape kDfmaShapes[] = {ELPA_DFMA_SHAPES(ELPA_SHAPE_ENTRY)};
+// The DFMA kernel (kernel_dfma.cuh) is compiled for nbw = 8/16/32/64, fused
+// group sizes k = 2/4/6/8 and CW = 2 warps (64 columns) per CTA.
+bool dfma_compiled(int64_t nbw, int kf, int CW) {
+    return (nbw == 8 || nbw == 16 || nbw == 32 || nbw == 64) && (kf == 2 || kf == 4 || kf == 6 || kf == 8) && CW == 2;
+}
 
 #define ELPA_SMALL_SHAPES(X) X(2, 2, 2, 1) X(1, 2, 2, 1)
 constexpr Shape kSmallShapes[] = {ELPA_SMALL_SHAPES(ELPA_SHAPE_ENTRY)};
 
-bool shape_compiled(bool dfma, int D, int CW, int NCT, int K);
-bool shape_compiled(bool dfma, int D, int CW, int NCT, int K, int b8) {
+bool shape_compiled(int D, int CW, int NCT, int K);
+bool shape_compiled(int D, int CW, int NCT, int K, int b8) {
     if (!b8_full_menu(b8)) {
         for (const Shape &s : kSmallShapes)
             if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
         return false;
     }
-    return shape_compiled(dfma, D, CW, NCT, K);
+    return shape_compiled(D, CW, NCT, K);
 }
 
-bool shape_compiled(bool dfma, int D, int CW, int NCT, int K) {
-    if (dfma) {
-        for (const Shape &s : kDfmaShapes)
-            if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
-        return false;
-    }
+bool shape_compiled(int D, int CW, int NCT, int K) {
     for (const Shape &s : kShapes)
         if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
     return false;
 }
 
-size_t dmma_smem(int b8, int D, int CW, int NCT, int K, int kind) {
-    const size_t blob = size_t(blob_doubles(b8 + 1, kind));
+size_t dmma_smem(int b8, int D, int CW, int NCT, int K) {
+    const size_t blob = size_t(blob_doubles(b8 + 1, 0));
     const int stages = (K * D * blob * 8 * 3 <= 100 * 1024) ? 3 : 2;
     return size_t(stages) * K * D * blob * 8 + size_t(2) * D * K * CW * NCT * 64 * 8 +
            size_t(2) * K * CW * NCT * 64 * 8 + 64;
+}
+
+// DFMA workspace: the prepared groups, then the group-base table (M + 1 int64)
+int64_t dfma_total_groups(int64_t n, int64_t nbw, int kf) {
+    const int64_t M = num_depths(n, nbw);
+    int64_t t = 0;
+    for (int64_t m = 0; m < M; m++) t += dfma_groups(n, nbw, kf, m);
+    return t;
 }
 
 // Automatic choice (measured sweeps in profiles/shape_sweep_r01*.jsonl):
@@ -111,28 +120,48 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     if (kernel < ELPA_B200_KERNEL_AUTO || kernel > ELPA_B200_KERNEL_DFMA) return ELPA_B200_ERR_ARG;
     if (kernel == ELPA_B200_KERNEL_AUTO)
         kernel = b8_supported(nbw) ? ELPA_B200_KERNEL_DMMA : ELPA_B200_KERNEL_REFERENCE;
-    if ((kernel == ELPA_B200_KERNEL_DMMA || kernel == ELPA_B200_KERNEL_DFMA) && !b8_supported(nbw))
-        return ELPA_B200_ERR_ARG;
+    if (kernel == ELPA_B200_KERNEL_DMMA && !b8_supported(nbw)) return ELPA_B200_ERR_ARG;
     p.kernel = kernel;
+    p.nbw = nbw;
     if (kernel == ELPA_B200_KERNEL_REFERENCE) {
         p.threads = 128;
         p.grid = (nev + 127) / 128;
         p.ws_bytes = 0;
         return ELPA_B200_OK;
     }
+    const int64_t M = num_depths(n, nbw);
+    if (kernel == ELPA_B200_KERNEL_DFMA) {
+        // lane-per-column FP64 CUDA-core kernel: k reflectors fused per group (fused_k, default
+        // 8: measured best of 2/4/6/8), CW = 2 warps per CTA
+        const int kf = (o && o->fused_k) ? o->fused_k : 8;
+        const int CW = (o && o->col_warps) ? o->col_warps : 2;
+        if ((o && (o->depth_warps > 1 || o->tiles_per_warp > 1 || o->groups_per_step > 1)) || !dfma_compiled(nbw, kf, CW))
+            return ELPA_B200_ERR_ARG;
+        p.kf = kf; p.CW = CW; p.D = 1; p.NCT = 1; p.K = 1;
+        p.grid_req = o ? o->grid_ctas : 0;
+        if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
+        p.nx = (nev + 32 * CW - 1) / (32 * CW);
+        p.items = p.nx * M;
+        p.grid = p.items;
+        p.threads = 32 * CW;
+        p.smem = size_t(4) * dfma_blob_doubles(int(nbw), kf) * 8 + 2 * 4 * 8 + 16;   // DfmaCfg::SMEM
+        const int64_t blobs = (M > 0) ? dfma_total_groups(n, nbw, kf) * dfma_blob_doubles(int(nbw), kf) * 8 : 0;
+        p.gb_off = (blobs + 255) / 256 * 256;
+        p.ws_bytes = (M > 0) ? p.gb_off + (M + 1) * 8 : 0;
+        return ELPA_B200_OK;
+    }
+    if (o && o->fused_k) return ELPA_B200_ERR_ARG;           // fused_k is a DFMA-kernel knob
     p.b8 = int(nbw / 8);
     const int64_t ntile = (nev + 7) / 8;
-    const int64_t M = num_depths(n, nbw);
     int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NCT = o ? o->tiles_per_warp : 0;
     int K = o ? o->groups_per_step : 0;
     if (D == 0 && CW == 0 && NCT == 0) {
         int Ka = 0;
         auto_shape(ntile, M, p.b8, D, CW, NCT, Ka);
-        if (kernel == ELPA_B200_KERNEL_DFMA) { D = 1; CW = 2; NCT = 2; }   // in the DFMA menu
         if (K == 0) K = Ka;
     }
     if (K == 0) K = 1;
-    if (!shape_compiled(kernel == ELPA_B200_KERNEL_DFMA, D, CW, NCT, K, p.b8)) return ELPA_B200_ERR_ARG;
+    if (!shape_compiled(D, CW, NCT, K, p.b8)) return ELPA_B200_ERR_ARG;
     p.D = D; p.CW = CW; p.NCT = NCT; p.K = K;
     p.grid_req = o ? o->grid_ctas : 0;
     if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
@@ -140,9 +169,9 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     p.items = p.nx * ((M + D - 1) / D);
     p.grid = p.items;          // capped by co-residency at launch
     p.threads = 32 * D * CW;
-    p.smem = dmma_smem(p.b8, D, CW, NCT, K, kernel == ELPA_B200_KERNEL_DFMA);
+    p.smem = dmma_smem(p.b8, D, CW, NCT, K);
     if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;   // shape does not fit this nbw
-    p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1, kernel == ELPA_B200_KERNEL_DFMA) * 8 : 0;
+    p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1, 0) * 8 : 0;
     return ELPA_B200_OK;
 }
 
@@ -157,13 +186,64 @@ int validate(int64_t n, int64_t nbw, int64_t nev, const void *hh_v, const void *
 }
 
 template <int B8>
-int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws, int kind, cudaStream_t s) {
+int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws, cudaStream_t s) {
     const int64_t M = num_depths(n, 8 * B8);
     const int64_t G0 = groups_at_depth(n, B8, 0);
     dim3 grid(unsigned((G0 + 3) / 4), unsigned(M));
-    if (kind == 1) prep_dmma_kernel<B8, 1><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
-    else prep_dmma_kernel<B8, 0><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
+    prep_dmma_kernel<B8, 0><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+}
+
+template <int B, int KF>
+int launch_prep_dfma(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, char *ws, cudaStream_t s) {
+    const int64_t M = num_depths(n, B);
+    int64_t *gbase = reinterpret_cast<int64_t *>(ws + p.gb_off);
+    dfma_gbase_kernel<<<1, 1, 0, s>>>(n, B, KF, M, gbase);
+    const int64_t G0 = dfma_groups(n, B, KF, 0);
+    dim3 grid(unsigned(std::min<int64_t>(64, (G0 * dfma_blob_doubles(B, KF) + 255) / 256)), unsigned(M));
+    prep_dfma_kernel<B, KF><<<grid, 256, 0, s>>>(n, hh_v, hh_tau, gbase, reinterpret_cast<double *>(ws));
+    return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+}
+
+template <int B, int KF, int CW>
+int launch_dfma(const Plan &p, int64_t n, int64_t nev, const char *ws, double *Q, int64_t ldq, cudaStream_t s) {
+    auto kern = apply_dfma_kernel<B, KF, CW>;
+    const size_t smem = DfmaCfg<B, KF, CW>::SMEM;
+    int per_sm = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DfmaCfg<B, KF, CW>::THREADS, smem) != cudaSuccess ||
+        per_sm < 1)
+        return fail_cuda();
+    int64_t grid = int64_t(per_sm) * sm_count();
+    if (p.grid_req > 0 && p.grid_req < grid) grid = p.grid_req;
+    if (grid > p.items) grid = p.items;
+    uint64_t *prog = nullptr;
+    const size_t pbytes = size_t(p.items + 1) * 8;
+    if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
+    int rc = cudaMemsetAsync(prog, 0, pbytes, s) == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+    if (rc == ELPA_B200_OK) {
+        kern<<<unsigned(grid), DfmaCfg<B, KF, CW>::THREADS, smem, s>>>(
+            n, nev, reinterpret_cast<const double *>(ws), reinterpret_cast<const int64_t *>(ws + p.gb_off), Q, ldq,
+            prog, pub_period());
+        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    }
+    if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    return rc;
+}
+
+// dispatch over the compiled (nbw, k) menu of the DFMA kernel (CW = 2)
+template <class F>
+int dfma_dispatch(int64_t nbw, int kf, F &&f) {
+#define ELPA_DFMA_K(B_)                                                          \
+    if (nbw == B_) {                                                             \
+        if (kf == 2) return f(std::integral_constant<int, B_>{}, std::integral_constant<int, 2>{}); \
+        if (kf == 4) return f(std::integral_constant<int, B_>{}, std::integral_constant<int, 4>{}); \
+        if (kf == 6) return f(std::integral_constant<int, B_>{}, std::integral_constant<int, 6>{}); \
+        if (kf == 8) return f(std::integral_constant<int, B_>{}, std::integral_constant<int, 8>{}); \
+    }
+    ELPA_DFMA_K(8) ELPA_DFMA_K(16) ELPA_DFMA_K(32) ELPA_DFMA_K(64)
+#undef ELPA_DFMA_K
+    return ELPA_B200_ERR_ARG;
 }
 
 // Grid of the persistent item kernel: the co-resident maximum (more CTAs could not run
@@ -214,34 +294,25 @@ int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, doub
 #define ELPA_SHAPE(D_, CW_, NCT_, K_)                          \
     if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
         return launch_dmma_shape<KIND_DMMA, B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
-#define ELPA_DFMA_SHAPE(D_, CW_, NCT_, K_)                     \
-    if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
-        return launch_dmma_shape<KIND_DFMA, B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
     if constexpr (B8 == 1 || B8 == 2 || B8 == 4 || B8 == 8) {
-        if (p.kernel == ELPA_B200_KERNEL_DFMA) {
-            ELPA_DFMA_SHAPES(ELPA_DFMA_SHAPE)
-        } else {
-            ELPA_SHAPES(ELPA_SHAPE)
-        }
+        ELPA_SHAPES(ELPA_SHAPE)
     } else {
-        if (p.kernel == ELPA_B200_KERNEL_DFMA) {
-            ELPA_SMALL_SHAPES(ELPA_DFMA_SHAPE)
-        } else {
-            ELPA_SMALL_SHAPES(ELPA_SHAPE)
-        }
+        ELPA_SMALL_SHAPES(ELPA_SHAPE)
     }
 #undef ELPA_SHAPE
-#undef ELPA_DFMA_SHAPE
     return ELPA_B200_ERR_ARG;
 }
 
 int prepare_impl(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, void *ws, cudaStream_t s) {
     if (p.kernel == ELPA_B200_KERNEL_REFERENCE || p.ws_bytes == 0) return ELPA_B200_OK;
+    if (p.kernel == ELPA_B200_KERNEL_DFMA)
+        return dfma_dispatch(p.nbw, p.kf, [&](auto b, auto k) {
+            return launch_prep_dfma<decltype(b)::value, decltype(k)::value>(p, n, hh_v, hh_tau, static_cast<char *>(ws), s);
+        });
     double *w = static_cast<double *>(ws);
-    const int kind = p.kernel == ELPA_B200_KERNEL_DFMA ? 1 : 0;
     switch (p.b8) {
 #define ELPA_PREP_CASE(B8_) \
-    case B8_: return launch_prep<B8_>(n, hh_v, hh_tau, w, kind, s);
+    case B8_: return launch_prep<B8_>(n, hh_v, hh_tau, w, s);
         ELPA_PREP_CASE(1) ELPA_PREP_CASE(2) ELPA_PREP_CASE(3) ELPA_PREP_CASE(4) ELPA_PREP_CASE(5) ELPA_PREP_CASE(6)
         ELPA_PREP_CASE(7) ELPA_PREP_CASE(8) ELPA_PREP_CASE(9) ELPA_PREP_CASE(10) ELPA_PREP_CASE(11)
         ELPA_PREP_CASE(12) ELPA_PREP_CASE(13) ELPA_PREP_CASE(14) ELPA_PREP_CASE(15) ELPA_PREP_CASE(16)
@@ -256,6 +327,11 @@ int apply_impl(const Plan &p, int64_t n, int64_t nbw, int64_t nev, const double 
         apply_reference_kernel<<<unsigned(p.grid), p.threads, 0, s>>>(n, nbw, nev, hh_v, hh_tau, Q, ldq);
         return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
     }
+    if (p.kernel == ELPA_B200_KERNEL_DFMA)
+        return dfma_dispatch(p.nbw, p.kf, [&](auto b, auto k) {
+            return launch_dfma<decltype(b)::value, decltype(k)::value, 2>(p, n, nev, static_cast<const char *>(ws), Q,
+                                                                         ldq, s);
+        });
     const double *w = static_cast<const double *>(ws);
     switch (p.b8) {
 #define ELPA_APPLY_CASE(B8_) \
@@ -343,9 +419,10 @@ int elpa_b200_describe(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts
     int rc = make_plan(n, nbw, nev, opts, p);
     if (rc != ELPA_B200_OK) return rc;
     if (buf && buflen)
-        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NCT=%d K=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
+        snprintf(buf, buflen,
+                 "kernel=%s b8=%d D=%d CW=%d NCT=%d K=%d k=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
                  p.kernel == ELPA_B200_KERNEL_DMMA ? "dmma" : (p.kernel == ELPA_B200_KERNEL_DFMA ? "dfma" : "reference"),
-                 p.b8, p.D, p.CW, p.NCT, p.K, (long long)p.items,
+                 p.b8, p.D, p.CW, p.NCT, p.K, p.kernel == ELPA_B200_KERNEL_DFMA ? p.kf : 8, (long long)p.items,
                  p.grid_req, p.threads, p.smem, (long long)p.ws_bytes);
     if (hh_total(n, nbw) == 0 || nev == 0) return 0;
     return p.kernel == ELPA_B200_KERNEL_REFERENCE ? 1 : 2;
@@ -609,10 +686,9 @@ std::vector<elpa_b200_opts> autotune_candidates(int64_t n, int64_t nbw, int64_t 
         return o;
     };
     const bool dmma = b8_supported(nbw);
-    if (dmma) {
-        c.push_back(mk(ELPA_B200_KERNEL_DMMA, 0, 0, 0));
-        c.push_back(mk(ELPA_B200_KERNEL_DFMA, 0, 0, 0));
-    }
+    const bool dfma = dfma_compiled(nbw, 8, 2);
+    if (dmma) c.push_back(mk(ELPA_B200_KERNEL_DMMA, 0, 0, 0));
+    if (dfma) c.push_back(mk(ELPA_B200_KERNEL_DFMA, 0, 0, 0));
     // the bit-exact reference kernel is a candidate only where it can finish quickly
     if (!dmma || double(hh_total(n, nbw)) * double(nev) * double(nbw) < 2e9)
         c.push_back(mk(ELPA_B200_KERNEL_REFERENCE, 0, 0, 0));
@@ -627,7 +703,11 @@ std::vector<elpa_b200_opts> autotune_candidates(int64_t n, int64_t nbw, int64_t 
         };
         if (b8_full_menu(b8)) {
             add(kShapes, sizeof(kShapes) / sizeof(kShapes[0]), ELPA_B200_KERNEL_DMMA);
-            add(kDfmaShapes, sizeof(kDfmaShapes) / sizeof(kDfmaShapes[0]), ELPA_B200_KERNEL_DFMA);
+            for (int kf : {2, 4, 6}) {                  // the DFMA kernel's fused-reflector count
+                elpa_b200_opts o = mk(ELPA_B200_KERNEL_DFMA, 0, 0, 0);
+                o.fused_k = kf;
+                if (dfma) c.push_back(o);
+            }
         } else {
             add(kSmallShapes, sizeof(kSmallShapes) / sizeof(kSmallShapes[0]), ELPA_B200_KERNEL_DMMA);
         }
@@ -822,12 +902,12 @@ int elpa_b200_autotune_run(int64_t n, int64_t nbw, int64_t nev, const double *hh
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) rc = fail_cuda();
-    void *ws[2] = {nullptr, nullptr};               // prepared reflectors per kernel kind
+    void *ws[5] = {};                               // prepared reflectors: DMMA, DFMA k = 2/4/6/8
     elpa_b200_opts o;
     while (rc == ELPA_B200_OK && elpa_b200_autotune_step(at, &o) == 1) {
         Plan p;
         if ((rc = make_plan(n, nbw, nev, &o, p)) != ELPA_B200_OK) break;
-        const int kind = p.kernel == ELPA_B200_KERNEL_DFMA ? 1 : 0;
+        const int kind = p.kernel == ELPA_B200_KERNEL_DFMA ? p.kf / 2 : 0;
         if (p.kernel != ELPA_B200_KERNEL_REFERENCE && !ws[kind]) {
             if (lib_malloc_async(&ws[kind], size_t(p.ws_bytes), s) != cudaSuccess) {
                 rc = fail_cuda();

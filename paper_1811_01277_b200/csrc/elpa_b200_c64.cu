@@ -58,6 +58,7 @@ size_t z_smem(int b8, int D, int CW, int NZ) {
 
 int z_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, ZPlan &p) {
     int kernel = o ? o->kernel : ELPA_B200_KERNEL_AUTO;
+    if (o && o->fused_k) return ELPA_B200_ERR_ARG;          // a DFMA-kernel knob
     if (kernel != ELPA_B200_KERNEL_AUTO && kernel != ELPA_B200_KERNEL_REFERENCE && kernel != ELPA_B200_KERNEL_DMMA)
         return ELPA_B200_ERR_ARG;
     if (kernel == ELPA_B200_KERNEL_AUTO)

@@ -47,11 +47,10 @@ __host__ __device__ inline int64_t total_groups(int64_t n, int64_t b8, int64_t M
     return group_base(n, b8, M);
 }
 // doubles per prepared group.  DMMA layout (kind 0): dot B-fragments of U = -V T (lambda x 32
-// lanes x 2), update B-fragments of V (same).  DFMA layout (kind 1): V row-major with a padded
-// row stride of 10 doubles (8*lambda rows), then -T^T row-major 8 x 8.
-// Complex layout (kind 2): B-fragments of Re U', Im U', Re V, Im V (4 x 64 lambda).
+// lanes x 2), update B-fragments of V (same).  Complex layout (kind 2): B-fragments of Re U',
+// Im U', Re V, Im V (4 x 64 lambda).
 __host__ __device__ inline int64_t blob_doubles(int64_t lambda, int kind = 0) {
-    return kind == 0 ? 128 * lambda : (kind == 1 ? 80 * lambda + 64 : 256 * lambda);
+    return kind == 0 ? 128 * lambda : 256 * lambda;
 }
 
 }  // namespace elpa_b200

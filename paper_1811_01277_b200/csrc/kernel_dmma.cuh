@@ -24,8 +24,8 @@
 //     warp (warp 0 already carries the HBM intake, the item dequeue and the progress publish).
 //   * Interior chunks (inside the matrix, every column valid) take a load/store fast path
 //     without bounds logic; only the first/last chunks and the last tile group pay for it.
-//   * KIND_ZMMA runs complex Hermitian tiles (NEXT-3) as (Re, Im) real tile pairs, and
-//     KIND_DFMA the same groups on the FP64 CUDA cores (the measured alternative).
+//   * KIND_ZMMA runs complex Hermitian tiles (NEXT-3) as (Re, Im) real tile pairs.  The FP64
+//     CUDA-core alternative is a separate kernel (kernel_dfma.cuh).
 #pragma once
 #include <type_traits>
 
@@ -140,7 +140,7 @@ __device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
 // q[t][i] in the m8n8k4 accumulator layout (lane l: rows 8i + 2(l%4) + {0,1} of column l/4).
 // Two policies compute the same compact-WY group, Q_W <- Q_W - V_g T^T V_g^T Q_W:
 // ---------------------------------------------------------------------------------------
-enum { KIND_DMMA = 0, KIND_DFMA = 1, KIND_ZMMA = 2 };
+enum { KIND_DMMA = 0, KIND_ZMMA = 2 };
 
 // FP64 tensor cores: 2*LAM + 2*LAM DMMA.8x8x4 per tile, no shuffles.  Blob layout (prep
 // kernel): dot B-fragments of U = -V_g T [LAM][32 lanes][2], update B-fragments of V_g
@@ -194,86 +194,6 @@ struct DmmaGroup {
                 dmma(q[t][i].x, q[t][i].y, w[t].y, ub.y);
             }
         }
-    }
-};
-
-// FP64 CUDA cores (DFMA): lane l holds rows 2(l%4)+{0,1} of every chunk of column l/4, forms
-// partial V^T q over its rows, reduces over the 4 lanes of the column with 2 butterfly
-// shuffles, applies -T^T redundantly per lane, then updates its rows.  Same flops as the DMMA
-// policy (+ the triangular T step), but 32-lane FMAs instead of 8x8x4 tiles.  Blob layout:
-// V row-major [8*LAM rows][VST = 10] (padding makes the 4 row-groups of a warp hit distinct
-// bank groups), then M = -T^T row-major [8][8].
-template <int LAM, int NCT>
-struct DfmaGroup {
-    static constexpr int VST = 10;
-    static constexpr int BLOB = 8 * LAM * VST + 64;
-    __device__ __forceinline__ static void apply(double2 (&q)[NCT][LAM], const double *blob, uint32_t tilemask,
-                                                 int lane) {
-        const int rho = lane & 3;
-        double y[NCT][8];
-#pragma unroll
-        for (int t = 0; t < NCT; t++)
-#pragma unroll
-            for (int a = 0; a < 8; a++) y[t][a] = 0.0;
-#pragma unroll
-        for (int i = 0; i < LAM; i++)
-#pragma unroll
-            for (int r = 0; r < 2; r++) {
-                const double2 *vr = reinterpret_cast<const double2 *>(blob + (8 * i + 2 * rho + r) * VST);
-                double v[8];
-#pragma unroll
-                for (int m = 0; m < 4; m++) {
-                    const double2 vv = vr[m];
-                    v[2 * m] = vv.x;
-                    v[2 * m + 1] = vv.y;
-                }
-#pragma unroll
-                for (int t = 0; t < NCT; t++) {
-                    if (!((tilemask >> t) & 1)) continue;
-                    const double qq = r ? q[t][i].y : q[t][i].x;
-#pragma unroll
-                    for (int a = 0; a < 8; a++) y[t][a] = fma(v[a], qq, y[t][a]);
-                }
-                asm volatile("" ::: "memory");   // keep each row's V loads next to their FMAs
-            }
-#pragma unroll
-        for (int t = 0; t < NCT; t++)
-#pragma unroll
-            for (int a = 0; a < 8; a++) {
-                y[t][a] += __shfl_xor_sync(0xffffffffu, y[t][a], 1);
-                y[t][a] += __shfl_xor_sync(0xffffffffu, y[t][a], 2);
-            }
-        const double *M = blob + 8 * LAM * VST;        // M[a][a'] = -T[a'][a], zero for a' > a
-        double w[NCT][8];
-#pragma unroll
-        for (int a = 0; a < 8; a++) {
-#pragma unroll
-            for (int t = 0; t < NCT; t++) w[t][a] = 0.0;
-#pragma unroll
-            for (int b = 0; b <= a; b++) {
-                const double mab = M[8 * a + b];
-#pragma unroll
-                for (int t = 0; t < NCT; t++) w[t][a] = fma(mab, y[t][b], w[t][a]);
-            }
-        }
-#pragma unroll
-        // Q_W += V_g W', reflector pairs outermost: each element still sums a = 0..7 in order,
-        // but the 2*LAM rows give independent chains without keeping every row's V live
-        for (int ap = 0; ap < 4; ap++)
-#pragma unroll
-            for (int i = 0; i < LAM; i++)
-#pragma unroll
-                for (int r = 0; r < 2; r++) {
-                    const double2 vv = reinterpret_cast<const double2 *>(blob + (8 * i + 2 * rho + r) * VST)[ap];
-#pragma unroll
-                    for (int t = 0; t < NCT; t++) {
-                        if (!((tilemask >> t) & 1)) continue;
-                        double acc = r ? q[t][i].y : q[t][i].x;
-                        acc = fma(vv.x, w[t][2 * ap], acc);
-                        acc = fma(vv.y, w[t][2 * ap + 1], acc);
-                        if (r) q[t][i].y = acc; else q[t][i].x = acc;
-                    }
-                }
     }
 };
 
@@ -342,9 +262,7 @@ struct ZmmaGroup {
 };
 
 template <int KIND, int LAM, int NCT>
-using GroupOf = typename std::conditional<
-    KIND == KIND_DMMA, DmmaGroup<LAM, NCT>,
-    typename std::conditional<KIND == KIND_DFMA, DfmaGroup<LAM, NCT>, ZmmaGroup<LAM, NCT>>::type>::type;
+using GroupOf = typename std::conditional<KIND == KIND_DMMA, DmmaGroup<LAM, NCT>, ZmmaGroup<LAM, NCT>>::type;
 
 // Complex Q I/O (interleaved re/im doubles): a lane's complex rows r, r+1 of one column as the
 // real tile pair (Re rows r, r+1), (Im rows r, r+1); rows outside [0, n) read as zero and are
@@ -391,11 +309,10 @@ struct DmmaCfg {
     static constexpr size_t SMEM_HAND = size_t(2) * D * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
     static constexpr size_t SMEM = SMEM_BLOBS + SMEM_HAND + SMEM_INTAKE + 64;
-    // Occupancy intent as a launch bound.  DMMA: the register window (4*LAM*NCT) + ~80, so an
+    // Occupancy intent as a launch bound: the register window (4*LAM*NCT) + ~80, so an
     // incidental code change cannot let ptxas spread into a CTA/SM fewer (seen: 138 -> 183
-    // registers, 3 -> 2 CTAs/SM, 28.1 -> 21.0 TF/s).  DFMA: cap near 168 (unbounded, ptxas
-    // hoists every shared V load of a group and spills ~1 KB).
-    static constexpr int REG_EST = (KIND == KIND_DFMA) ? 168 : 4 * LAM * NCT + 80 + (KIND == KIND_ZMMA ? 16 : 0);
+    // registers, 3 -> 2 CTAs/SM, 28.1 -> 21.0 TF/s).
+    static constexpr int REG_EST = 4 * LAM * NCT + 80 + (KIND == KIND_ZMMA ? 16 : 0);
     static constexpr int MINB_RAW = 65536 / (THREADS * REG_EST);
     static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
 };

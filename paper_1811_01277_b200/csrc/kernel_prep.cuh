@@ -9,7 +9,6 @@
 //   dotB[i][lane] = (U[8i + 2(lane%4)][lane/4],  U[8i + 2(lane%4) + 1][lane/4])
 //   updB[i][lane] = (V[8i + lane/4][2(lane%4)],  V[8i + lane/4][2(lane%4) + 1])
 // One warp per group.  Missing reflectors (j < 0 or j > J_m) get tau = 0 (identity).
-// KIND 1 (DFMA kernel) instead writes V row-major with row stride 10 and M = -T^T row-major.
 #pragma once
 #include "geometry.cuh"
 
@@ -70,14 +69,6 @@ prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__res
         __syncwarp();
     }
     double *blob = blobs + (group_base(n, B8, m) + g) * blob_doubles(LAM, KIND);
-    if (KIND == 1) {
-        for (int idx = lane; idx < WR * 10; idx += 32) {
-            const int w = idx / 10, a = idx % 10;
-            blob[idx] = (a < 8) ? V[w][a] : 0.0;
-        }
-        for (int e = lane; e < 64; e += 32) blob[WR * 10 + e] = -Ts[warp][e & 7][e >> 3];
-        return;
-    }
     // U = -V T (window rows x 8): the dot phase then yields W^T = Q_W^T U directly
     // (W = -T^T V^T Q_W), so the apply kernel needs no separate T step
     auto U = [&](int w, int a) {

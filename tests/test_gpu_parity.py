@@ -278,22 +278,46 @@ def test_multi_item_ctas_at_scale(eb, shape, grid):
     assert _rel(got, want) <= TOL
 
 
-DFMA_SHAPES = [(1, 2, 2, 1), (2, 2, 2, 1), (1, 4, 2, 1), (2, 4, 2, 1), (1, 2, 4, 1), (2, 2, 4, 1)]
-
-
-@pytest.mark.parametrize("shape", DFMA_SHAPES)
-@pytest.mark.parametrize("nbw", [8, 32, 64])
-def test_dfma_kernel_shapes(eb, shape, nbw):
-    """The DFMA comparison kernel (same groups, schedule and items on CUDA cores)."""
-    D, CW, NCT, K = shape
+@pytest.mark.parametrize("kf", [2, 4, 6, 8])
+@pytest.mark.parametrize("nbw", [8, 16, 32, 64])
+def test_dfma_kernel_fused_k(eb, kf, nbw):
+    """The FP64 CUDA-core kernel (lane owns a column, k = fused_k reflectors per group applied
+    in sequence to a register window; north_star item 3) against the oracle, ragged n and nev,
+    one CTA (every item in order), two CTAs (depth items chained through the progress words)
+    and all co-resident CTAs."""
     n, nev = 301, 45
-    hv, tau, s, L, Q = synth_case(n, nbw, nev, nbw * 7 + D, ldq=302)
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, nbw * 7 + kf, ldq=302)
     want = oracle.apply(hv, tau, s, L, Q)
-    for grid in (0, 2):
-        got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DFMA, depth_warps=D, col_warps=CW,
-                                                         tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
-        assert _rel(got[:, :n], want[:, :n]) <= TOL, (shape, grid)
+    for grid in (0, 1, 2):
+        got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DFMA, fused_k=kf, grid_ctas=grid))
+        assert _rel(got[:, :n], want[:, :n]) <= TOL, (kf, grid)
         assert np.array_equal(got[:, n:], Q[:, n:])
+
+
+@pytest.mark.parametrize("kf", [2, 8])
+@pytest.mark.parametrize("n,nbw,nev", [(3, 8, 3), (10, 8, 10), (17, 16, 17), (66, 64, 66), (130, 64, 130),
+                                       (2049, 64, 77), (1000, 32, 200)])
+def test_dfma_kernel_edge_sizes(eb, kf, n, nbw, nev):
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 71 + n)
+    want = oracle.apply(hv, tau, s, L, Q)
+    got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DFMA, fused_k=kf))
+    assert _rel(got, want) <= TOL
+
+
+def test_dfma_kernel_rejects_unsupported(eb):
+    """fused_k outside 2/4/6/8, nbw outside 8/16/32/64, DMMA-only shape knobs, and fused_k on
+    another kernel are ERR_ARG before any launch."""
+    n, nbw, nev = 200, 32, 16
+    hv, tau, s, L, Q = synth_case(n, nbw, nev, 5)
+    for opts in (dict(kernel=eb.KERNEL_DFMA, fused_k=3), dict(kernel=eb.KERNEL_DFMA, fused_k=10),
+                 dict(kernel=eb.KERNEL_DFMA, depth_warps=2), dict(kernel=eb.KERNEL_DMMA, fused_k=4)):
+        with pytest.raises(eb.ElpaB200Error) as ei:
+            run_gpu(eb, n, nbw, hv, tau, Q, opts=opts)
+        assert ei.value.code == eb.ERR_ARG
+    hv, tau, s, L, Q = synth_case(n, 24, nev, 5)
+    with pytest.raises(eb.ElpaB200Error) as ei:
+        run_gpu(eb, n, 24, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DFMA))
+    assert ei.value.code == eb.ERR_ARG
 
 
 def test_dfma_real_C1_residual(eb):
@@ -368,10 +392,11 @@ def test_progress_publish_multi_column_warps(eb, shape, grid):
     n, nbw, nev = 700, 64, CW * NCT * 8          # one tile group: all items chain on one x
     hv, tau, s, L, Q = synth_case(n, nbw, nev, 41 + grid)
     want = oracle.apply(hv, tau, s, L, Q)
-    for kernel in (2, 3) if shape in [(1, 2, 4, 1), (2, 2, 2, 1), (1, 4, 2, 1), (2, 2, 4, 1)] else (2,):
-        got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=kernel, depth_warps=D, col_warps=CW,
-                                                         tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
-        assert _rel(got, want) <= TOL, kernel
+    got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
+                                                     tiles_per_warp=NCT, grid_ctas=grid, groups_per_step=K))
+    assert _rel(got, want) <= TOL
+    got = run_gpu(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DFMA, grid_ctas=grid))
+    assert _rel(got, want) <= TOL
 
 
 def test_autotune_run_and_use_best(eb):
