@@ -140,7 +140,7 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
         p.kf = kf; p.CW = CW; p.D = 1; p.NCT = 1; p.K = 1;
         p.grid_req = o ? o->grid_ctas : 0;
         if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
-        p.nx = (nev + 32 * CW - 1) / (32 * CW);
+        p.nx = (nev + 16 * CW - 1) / (16 * CW);           // two lanes per column: 16 columns per warp
         p.items = p.nx * M;
         p.grid = p.items;
         p.threads = 32 * CW;

@@ -4,30 +4,43 @@
 // reflectors are fused in groups of k = 2/4/6/8 so each Q tile is reused k times ... reflectors
 // double-buffered into shared memory".  The ELPA kernels the paper speeds up apply 2/4/6
 // reflectors per pass in AVX-512 registers (prior art); here:
-//   * a lane owns one column of Q; a warp owns 32 consecutive columns, a CTA CW warps;
+//   * two lanes own one column of Q (16 columns per warp, CW warps per CTA), each holding half
+//     of the column's window rows in registers (row pairs, alternating between the two lanes):
+//     one lane cannot hold the nbw + k FP64 rows of its window without spilling at nbw = 64;
 //   * group g of depth m holds the KF sweeps j = KF*g + KF-2-a, a = 0..KF-1 (a = 0 is the
 //     highest sweep, applied first: reverse generation order within the group).  Reflector a
 //     starts at row KF*g + m*b + KF-1-a, so the group's rows are the window
-//     [KF*g + m*b, KF*g + m*b + b + KF), held in the lane's registers (b + KF doubles);
+//     [KF*g + m*b, KF*g + m*b + WP), WP >= b + KF;
 //   * the KF reflectors are applied one at a time, exactly the oracle's recurrence per column
-//     (w = tau v^T q, q -= w v) but with fused multiply-adds: each window row is loaded from
-//     HBM once per group and reused by the KF reflectors — the k-fold reuse of the paper's
-//     blocked kernels, with no compact-WY factor and no padding flops;
-//   * v is a warp-broadcast 16-byte shared-memory read (two rows per load, re-read for the
-//     update: keeping b doubles of v live would double the registers);
+//     (w = tau v^T q, q -= w v) but with fused multiply-adds: each lane forms its half of v^T q,
+//     one shuffle adds the halves, and each lane updates its rows.  Every window row is loaded
+//     from HBM once per group and reused by the KF reflectors — the k-fold reuse of the paper's
+//     blocked kernels — with no compact-WY factor;
+//   * v is laid out in the blob aligned to the window (zero outside the reflector) and read with
+//     warp-broadcast 16-byte shared-memory loads (two rows per load, re-read for the update);
 //   * groups run from the bottom of the matrix upward (g descending), the window sliding up by
-//     KF rows per group: the KF new top rows are prefetched into registers one group ahead,
-//     the KF bottom rows are written back.
+//     KF rows per group; the window is a register ring (no moves): the KF new top rows are
+//     prefetched one step ahead, the KF bottom rows are written back.
 // Work items, the dynamic dequeue and the progress words are those of the DMMA kernel
 // with one depth per item: item (x, m) consumes the rows item (x, m-1) has
 // finalised.  Progress is counted in rows: prog = n - r means every row >= r is final.
-// Blob per group (prep_dfma_kernel): v[a][0..b) (v_0 = 1, zero past L), then tau[a].
 #pragma once
 #include "kernel_dmma.cuh"
 
 namespace elpa_b200 {
 
-__host__ __device__ constexpr int dfma_blob_doubles(int b, int kf) { return kf * b + kf + (kf & 1); }
+// window rows: the smallest multiple of k that is >= b + k and a multiple of 4 (the row-pair
+// ring is split evenly between the two lanes of a column)
+__host__ __device__ constexpr int dfma_window(int b, int kf) {
+    int w = (b + kf + kf - 1) / kf * kf;
+    while (w % 4) w += kf;
+    return w;
+}
+// doubles per prepared group: per reflector the window-aligned vector twice over (2 WP: the
+// lanes' pair sequences wrap around the ring without an index wrap), then tau[KF], padded even
+__host__ __device__ constexpr int dfma_blob_doubles(int b, int kf) {
+    return kf * 2 * dfma_window(b, kf) + kf + (kf & 1);
+}
 
 // groups of depth m (sweeps j <= J_m = n-3-m*b, group g covers j <= KF*g + KF-2)
 __host__ __device__ inline int64_t dfma_groups(int64_t n, int64_t b, int64_t kf, int64_t m) {
@@ -44,11 +57,14 @@ __global__ void dfma_gbase_kernel(int64_t n, int64_t b, int64_t kf, int64_t M, i
     }
 }
 
-// one thread per blob element; grid (element blocks, M)
+// one thread per blob element; grid (element blocks, M).  Reflector a's vector occupies window
+// rows [KF-1-a, KF-1-a+L) (v_0 = 1), zero elsewhere, stored at [a*2WP, a*2WP + WP) and again at
+// [a*2WP + WP, (a+1)*2WP).
 template <int B, int KF>
 __global__ void __launch_bounds__(256)
 prep_dfma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__restrict__ hh_tau,
                  const int64_t *__restrict__ gbase, double *__restrict__ blobs) {
+    constexpr int WP = dfma_window(B, KF);
     constexpr int BLOB = dfma_blob_doubles(B, KF);
     const int64_t m = blockIdx.y;
     const int64_t G = dfma_groups(n, B, KF, m);
@@ -58,16 +74,17 @@ prep_dfma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__res
         const int64_t g = e / BLOB;
         const int w = int(e % BLOB);
         double val = 0.0;
-        if (w < KF * B) {
-            const int a = w / B, i = w % B;
+        if (w < KF * 2 * WP) {
+            const int a = w / (2 * WP), row = (w % (2 * WP)) % WP;
+            const int i = row - (KF - 1 - a);               // index into the reflector's vector
             const int64_t j = KF * g + KF - 2 - a;
-            if (j >= 0 && j <= Jm) {
+            if (j >= 0 && j <= Jm && i >= 0) {
                 const int64_t s = j + 1 + m * B;
                 const int64_t L = (n - s < B) ? (n - s) : B;
                 if (i < L) val = (i == 0) ? 1.0 : hh_v[(hh_off(j, n, B) + m) * B + i];
             }
-        } else if (w < KF * B + KF) {
-            const int a = w - KF * B;
+        } else if (w < KF * 2 * WP + KF) {
+            const int a = w - KF * 2 * WP;
             const int64_t j = KF * g + KF - 2 - a;
             if (j >= 0 && j <= Jm) val = hh_tau[hh_off(j, n, B) + m];
         }
@@ -95,15 +112,15 @@ __device__ __forceinline__ void dfma_static_for(F &&f) {
 
 template <int B, int KF, int CW>
 struct DfmaCfg {
-    static constexpr int WP = (B + KF + KF - 1) / KF * KF;  // window rows per lane (>= b + k, a multiple of k)
+    static constexpr int WP = dfma_window(B, KF);           // window rows
+    static constexpr int NPR = WP / 2;                      // row pairs of the window (ring slots)
+    static constexpr int NL = NPR / 2;                      // ring slots per lane
     static constexpr int NW = WP / KF;                      // steps a row spends in the window
     static constexpr int BLOB = dfma_blob_doubles(B, KF);
     static constexpr int THREADS = 32 * CW;
-    static constexpr int STAGES = 4;                       // blobs issued 2 steps ahead, 1 step slack
+    static constexpr int COLS = 16 * CW;                    // columns per CTA (two lanes per column)
+    static constexpr int STAGES = 4;                        // blobs issued 2 steps ahead, 1 step slack
     static constexpr size_t SMEM = size_t(STAGES) * BLOB * sizeof(double) + 2 * STAGES * 8 + 16;   // + barriers, item
-    // register cap: the window (2*WP) plus ~60; without it ptxas hoists the shared-memory loads
-    // of whole reflector passes and spills
-    static constexpr int REGCAP = (2 * WP + 64 + 7) / 8 * 8 > 255 ? 255 : (2 * WP + 64 + 7) / 8 * 8;
 };
 
 template <int B, int KF, int CW>
@@ -111,10 +128,10 @@ __global__ void __launch_bounds__((DfmaCfg<B, KF, CW>::THREADS))
 apply_dfma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, const int64_t *__restrict__ gbase,
                   double *Q, int64_t ldq, uint64_t *prog, int pub_period) {
     using Cfg = DfmaCfg<B, KF, CW>;
-    constexpr int WP = Cfg::WP;
-    constexpr int NW = Cfg::NW;
+    constexpr int WP = Cfg::WP, NPR = Cfg::NPR, NL = Cfg::NL, NW = Cfg::NW;
     constexpr int BLOB = Cfg::BLOB;
     constexpr int S = Cfg::STAGES;
+    constexpr int KP = KF / 2;                              // row pairs per step
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sblob = reinterpret_cast<double *>(smem_raw);                                  // [S][BLOB]
@@ -124,8 +141,9 @@ apply_dfma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
 
     const int n = int(n64), nev = int(nev64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h = lane & 1;                                 // which half of the column's rows
     const int M = int(num_depths(n64, B));
-    const int NX = (nev + 32 * CW - 1) / (32 * CW);
+    const int NX = (nev + Cfg::COLS - 1) / Cfg::COLS;
     const bool issuer = threadIdx.x == 32 * (CW - 1);
 
     if (threadIdx.x == 0) {
@@ -144,7 +162,7 @@ apply_dfma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         const int k = *s_item;
         if (k >= NX * M) break;
         const int m = k / NX, x = k % NX;
-        const int c = x * 32 * CW + warp * 32 + lane;
+        const int c = x * Cfg::COLS + warp * 16 + (lane >> 1);
         const bool ok = c < nev;
         double *qc = Q + int64_t(ok ? c : nev - 1) * ldq;
         const int G = int(dfma_groups(n64, B, KF, m));
@@ -186,13 +204,13 @@ apply_dfma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 return *reinterpret_cast<const double2 *>(qc + r);
             return make_double2(ld(r), ld(r + 1));
         };
-        auto st_pair = [&](int r, double x, double y) {
+        auto st_pair = [&](int r, double2 v) {
             if (!ok) return;
             if (r >= 0 && r + 2 <= n && ((reinterpret_cast<uintptr_t>(qc + r) & 15) == 0)) {
-                *reinterpret_cast<double2 *>(qc + r) = make_double2(x, y);
+                *reinterpret_cast<double2 *>(qc + r) = v;
             } else {
-                if (r >= 0 && r < n) qc[r] = x;
-                if (r + 1 >= 0 && r + 1 < n) qc[r + 1] = y;
+                if (r >= 0 && r < n) qc[r] = v.x;
+                if (r + 1 >= 0 && r + 1 < n) qc[r + 1] = v.y;
             }
         };
         // publish early once the emitted rows cover the next depth's first window (its item can
@@ -208,40 +226,41 @@ apply_dfma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
         //   below: by step NW every chunk came through the intake);
         //   after the group-0 step, NW - 1 drain steps emit the last window (zeros enter the top:
         //   rows above rowbase belong to earlier depths and are never read or written here).
-        // The window is a register ring: window row w of step t lives in q[(w - KF*t) mod WP], so
-        // the slide costs no register moves; the step loop is unrolled NW times (one body per
-        // rotation) so every ring index is a compile-time constant.
-        double q[WP];
+        // Ring: window row pair p of step t lives in slot s = (p - KP*t) mod NPR, slot s in lane
+        // (s & 1) of the column's lane pair at qh[s >> 1].  Lane h's slots 2l + h hold window pairs
+        // p = (2l + h + KP*r) mod NPR (r = t mod NW), i.e. v pairs c0 + 2l with c0 = (h + KP*r)
+        // mod NPR, read from the doubled vector without an index wrap.  The step loop is unrolled
+        // NW times so every ring index is a compile-time constant.
+        double2 qh[NL];
 #pragma unroll
-        for (int i = 0; i < WP; i++) q[i] = 0.0;
+        for (int i = 0; i < NL; i++) qh[i] = make_double2(0.0, 0.0);
         const int T = G + 2 * NW - 1;                       // steps of this item
         int top = rowbase + KF * (G - 1 + NW);
-        double nxt[KF];                                     // the next step's KF top rows
-        auto fetch = [&](int t) {                           // intake for step t (t >= 1)
-            const int r = top - KF;                         // top(t) = top(t-1) - KF
-            if (t <= G - 1 + NW) {                          // the group-0 step takes in real rows
-                await_rows(r);
+        double2 nxt[KP];                                    // the next step's top pairs (own slots only)
+        auto fetch = [&](auto rc_next, int t) {             // intake for step t (t >= 1), rotation of t
+            constexpr int r = decltype(rc_next)::value;
+            const int rr = top - KF;                        // top(t) = top(t-1) - KF
+            const bool real = t <= G - 1 + NW;              // the group-0 step takes in real rows
+            if (real) await_rows(rr);
 #pragma unroll
-                for (int i = 0; i < KF / 2; i++) {
-                    const double2 v = ld_pair(r + 2 * i);
-                    nxt[2 * i] = v.x;
-                    nxt[2 * i + 1] = v.y;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < KF; i++) nxt[i] = 0.0;
+            for (int i = 0; i < KP; i++) {
+                const int s = ((i - KP * r) % NPR + NPR) % NPR;
+                nxt[i] = (real && (s & 1) == h) ? ld_pair(rr + 2 * i) : make_double2(0.0, 0.0);
             }
         };
-        if (T > 1) fetch(1);
+        if (T > 1) fetch(std::integral_constant<int, 1 % NW>{}, 1);
         int pub_count = 0;
         auto step = [&](auto rc, int t) {
             constexpr int r = decltype(rc)::value;          // ring rotation of step t (t mod NW)
-            auto sl = [](int w) { return ((w - KF * r) % WP + WP) % WP; };
-            if (t > 0) {                                    // slide up by KF rows: take in the top rows
+            auto slot = [](int p) { return ((p - KP * r) % NPR + NPR) % NPR; };
+            if (t > 0) {                                    // slide up by KF rows: take in the top pairs
 #pragma unroll
-                for (int i = 0; i < KF; i++) q[sl(i)] = nxt[i];
+                for (int i = 0; i < KP; i++) {
+                    const int s = slot(i);
+                    if ((s & 1) == h) qh[s >> 1] = nxt[i];
+                }
                 top -= KF;
-                if (t + 1 < T) fetch(t + 1);
+                if (t + 1 < T) fetch(std::integral_constant<int, (r + 1) % NW>{}, t + 1);
             }
             const int g = G - 1 - (t - NW);
             if (g >= 0 && g < G) {
@@ -250,34 +269,37 @@ apply_dfma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
                 const int gs = gstep0 + st, stage = gs % S;
                 mbar_wait(&bars[stage], uint32_t((gs / S) & 1));
                 const double *blob = sblob + stage * BLOB;
-                const double *tau = blob + KF * B;
-#pragma unroll
+                const double *tau = blob + KF * 2 * WP;
+                const int c0 = (h + KP * r) % NPR;          // first v pair of this lane's slots
+                // the window-aligned blob makes the reflector body independent of a: one copy of it
+                // per rotation (the unrolled version missed the instruction cache, "no_instruction"
+                // 3.4 stalls per issue)
+#pragma unroll 1
                 for (int a = 0; a < KF; a++) {
-                    const int o = KF - 1 - a;
-                    const double2 *v2 = reinterpret_cast<const double2 *>(blob + a * B);
-                    // v is streamed from shared memory LA pairs ahead of its use (volatile loads: see
-                    // lds_v2), once for the dot and once for the update; 4 partial sums
-                    constexpr int NP = B / 2, LA = 4;
+                    const double2 *v2 = reinterpret_cast<const double2 *>(blob + a * 2 * WP) + c0;
+                    constexpr int LA = 8;                   // shared-memory loads in flight ahead of use
                     double2 vr[LA];
                     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int i = 0; i < LA && i < NP; i++) vr[i] = lds_v2(v2 + i);
+                    for (int i = 0; i < LA && i < NL; i++) vr[i] = lds_v2(v2 + 2 * i);
 #pragma unroll
-                    for (int i = 0; i < NP; i++) {
-                        const double2 vv = vr[i % LA];
-                        if (i + LA < NP) vr[i % LA] = lds_v2(v2 + i + LA);
-                        acc[2 * (i & 1)] = fma(vv.x, q[sl(o + 2 * i)], acc[2 * (i & 1)]);
-                        acc[2 * (i & 1) + 1] = fma(vv.y, q[sl(o + 2 * i + 1)], acc[2 * (i & 1) + 1]);
+                    for (int l = 0; l < NL; l++) {
+                        const double2 vv = vr[l % LA];
+                        if (l + LA < NL) vr[l % LA] = lds_v2(v2 + 2 * (l + LA));
+                        acc[2 * (l & 1)] = fma(vv.x, qh[l].x, acc[2 * (l & 1)]);
+                        acc[2 * (l & 1) + 1] = fma(vv.y, qh[l].y, acc[2 * (l & 1) + 1]);
                     }
-                    const double w = -tau[a] * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+                    double part = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                    part += __shfl_xor_sync(0xffffffffu, part, 1);  // both halves of v^T q
+                    const double w = -tau[a] * part;
 #pragma unroll
-                    for (int i = 0; i < LA && i < NP; i++) vr[i] = lds_v2(v2 + i);
+                    for (int i = 0; i < LA && i < NL; i++) vr[i] = lds_v2(v2 + 2 * i);
 #pragma unroll
-                    for (int i = 0; i < NP; i++) {
-                        const double2 vv = vr[i % LA];
-                        if (i + LA < NP) vr[i % LA] = lds_v2(v2 + i + LA);
-                        q[sl(o + 2 * i)] = fma(vv.x, w, q[sl(o + 2 * i)]);
-                        q[sl(o + 2 * i + 1)] = fma(vv.y, w, q[sl(o + 2 * i + 1)]);
+                    for (int l = 0; l < NL; l++) {
+                        const double2 vv = vr[l % LA];
+                        if (l + LA < NL) vr[l % LA] = lds_v2(v2 + 2 * (l + LA));
+                        qh[l].x = fma(vv.x, w, qh[l].x);
+                        qh[l].y = fma(vv.y, w, qh[l].y);
                     }
                 }
                 __syncwarp();
@@ -287,8 +309,10 @@ apply_dfma_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, 
             const int rb = top + WP - KF;
             if (rb < n) {
 #pragma unroll
-                for (int i = 0; i < KF / 2; i++)
-                    st_pair(rb + 2 * i, q[sl(WP - KF + 2 * i)], q[sl(WP - KF + 2 * i + 1)]);
+                for (int i = 0; i < KP; i++) {
+                    const int s = slot(NPR - KP + i);
+                    if ((s & 1) == h) st_pair(rb + 2 * i, qh[s >> 1]);
+                }
             }
             const bool pub = t + 1 < T && ((pub_count == pub_period - 1) || (early && rb <= next_top0));
             if (pub && rb <= next_top0) early = false;
