@@ -111,6 +111,10 @@ int elpa_b200_set_workspace_cache(int enable);
  * -1 if n < 0 or nbw < 1. */
 int64_t elpa_hh_count(int64_t n, int64_t nbw);
 
+/* off(j): generation index of the first reflector of sweep j (the reflectors of sweeps < j are
+ * rows [0, off(j)) of hh_v); R for j >= n - 2, 0 when R == 0; -1 on bad arguments. */
+int64_t elpa_hh_offset(int64_t n, int64_t nbw, int64_t j);
+
 /* One-shot device call: Q <- H_0 ... H_{R-1} Q, asynchronous on `stream`.
  * hh_v, hh_tau, Q are device pointers.  Returns ELPA_B200_OK or a negative code.
  * nev == 0 or R == 0 returns OK without touching memory. */
@@ -145,6 +149,16 @@ int64_t elpa_b200_workspace_bytes(int64_t n, int64_t nbw, const elpa_b200_opts *
 int elpa_b200_prepare(int64_t n, int64_t nbw, const double *hh_v, const double *hh_tau,
                       void *workspace, size_t workspace_bytes, elpa_b200_stream_t stream,
                       const elpa_b200_opts *opts);
+/* Chunked preparation (the multi-GPU path prepares while the broadcast of later reflectors is
+ * still in flight): prepares the reflector groups that are complete once the reflectors of every
+ * sweep j < sweep_hi are in hh_v/hh_tau and that were not complete for sweeps j < sweep_lo
+ * (sweep_lo = 0 on the first call).  A sequence of calls with sweep_lo = the previous sweep_hi,
+ * the last with sweep_hi >= n - 2, prepares the workspace exactly as elpa_b200_prepare does.
+ * Sweep j's reflectors are rows [off(j), off(j) + M_j) of hh_v: contiguous in generation order.
+ * ERR_ARG also when sweep_lo < 0 or sweep_hi < sweep_lo. */
+int elpa_b200_prepare_sweeps(int64_t n, int64_t nbw, const double *hh_v, const double *hh_tau,
+                             void *workspace, size_t workspace_bytes, int64_t sweep_lo, int64_t sweep_hi,
+                             elpa_b200_stream_t stream, const elpa_b200_opts *opts);
 /* opts.kernel and n, nbw must be the ones the workspace was prepared with: a workspace this
  * process prepared for another kernel, n or nbw is rejected with ELPA_B200_ERR_ARG (the library
  * remembers the last 256 prepared workspace pointers; others are not checked). */

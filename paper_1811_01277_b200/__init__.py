@@ -30,6 +30,10 @@ def _load():
     lib.elpa_b200_set_workspace_cache.argtypes = [i32]
     lib.elpa_hh_count.restype = i64
     lib.elpa_hh_count.argtypes = [i64, i64]
+    lib.elpa_hh_offset.restype = i64
+    lib.elpa_hh_offset.argtypes = [i64, i64, i64]
+    lib.elpa_b200_prepare_sweeps.restype = i32
+    lib.elpa_b200_prepare_sweeps.argtypes = [i64, i64, p, p, p, sz, i64, i64, p, p]
     lib.elpa_trans_ev_tridi_to_band.restype = i32
     lib.elpa_trans_ev_tridi_to_band.argtypes = [i64, i64, i64, p, p, p, i64, p]
     for f in (lib.elpa_trans_ev_tridi_to_band_ex, lib.elpa_trans_ev_tridi_to_band_host):
@@ -222,6 +226,23 @@ def prepare(n, nbw, hh_v, hh_tau, workspace, stream=None, opts=None):
     rc = _lib.elpa_b200_prepare(int(n), int(nbw), _dev_ptr(hh_v, "hh_v"), _dev_ptr(hh_tau, "hh_tau"),
                                 wptr, nbytes, s, op)
     _check(rc, "elpa_b200_prepare")
+
+
+def hh_offset(n, nbw, j):
+    """off(j): generation index of sweep j's first reflector (R for j >= n - 2)."""
+    return int(_lib.elpa_hh_offset(int(n), int(nbw), int(j)))
+
+
+def prepare_sweeps(n, nbw, hh_v, hh_tau, workspace, sweep_lo, sweep_hi, stream=None, opts=None):
+    """Chunked preparation (elpa_b200_prepare_sweeps): the groups complete for sweeps < sweep_hi
+    not yet complete for sweeps < sweep_lo."""
+    o, op = _opts_ptr(opts)
+    s = _stream_handle(stream, hh_v.device)
+    wptr = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None and workspace.numel() else None
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    rc = _lib.elpa_b200_prepare_sweeps(int(n), int(nbw), _dev_ptr(hh_v, "hh_v"), _dev_ptr(hh_tau, "hh_tau"), wptr,
+                                       nbytes, int(sweep_lo), int(sweep_hi), s, op)
+    _check(rc, "elpa_b200_prepare_sweeps")
 
 
 def apply_prepared(n, nbw, workspace, Q, hh_v=None, hh_tau=None, stream=None, opts=None):

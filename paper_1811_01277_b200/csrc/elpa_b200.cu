@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -185,23 +186,30 @@ int validate(int64_t n, int64_t nbw, int64_t nev, const void *hh_v, const void *
     return ELPA_B200_OK;
 }
 
+// groups [g_lo, g_hi) of every depth (g_hi < 0: all groups)
 template <int B8>
-int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws, cudaStream_t s) {
+int launch_prep(int64_t n, const double *hh_v, const double *hh_tau, double *ws, cudaStream_t s, int64_t g_lo = 0,
+                int64_t g_hi = -1) {
     const int64_t M = num_depths(n, 8 * B8);
     const int64_t G0 = groups_at_depth(n, B8, 0);
-    dim3 grid(unsigned((G0 + 3) / 4), unsigned(M));
-    prep_dmma_kernel<B8, 0><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws);
+    if (g_hi < 0 || g_hi > G0) g_hi = G0;
+    if (g_lo >= g_hi || M == 0) return ELPA_B200_OK;
+    dim3 grid(unsigned((g_hi - g_lo + 3) / 4), unsigned(M));
+    prep_dmma_kernel<B8, 0><<<grid, 128, 0, s>>>(n, hh_v, hh_tau, ws, g_lo, g_hi);
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
 }
 
 template <int B, int KF>
-int launch_prep_dfma(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, char *ws, cudaStream_t s) {
+int launch_prep_dfma(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, char *ws, cudaStream_t s,
+                     int64_t g_lo = 0, int64_t g_hi = -1) {
     const int64_t M = num_depths(n, B);
-    int64_t *gbase = reinterpret_cast<int64_t *>(ws + p.gb_off);
-    dfma_gbase_kernel<<<1, 1, 0, s>>>(n, B, KF, M, gbase);
     const int64_t G0 = dfma_groups(n, B, KF, 0);
-    dim3 grid(unsigned(std::min<int64_t>(64, (G0 * dfma_blob_doubles(B, KF) + 255) / 256)), unsigned(M));
-    prep_dfma_kernel<B, KF><<<grid, 256, 0, s>>>(n, hh_v, hh_tau, gbase, reinterpret_cast<double *>(ws));
+    if (g_hi < 0 || g_hi > G0) g_hi = G0;
+    int64_t *gbase = reinterpret_cast<int64_t *>(ws + p.gb_off);
+    if (g_lo == 0) dfma_gbase_kernel<<<1, 1, 0, s>>>(n, B, KF, M, gbase);
+    if (g_lo >= g_hi || M == 0) return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+    dim3 grid(unsigned(std::min<int64_t>(64, ((g_hi - g_lo) * dfma_blob_doubles(B, KF) + 255) / 256)), unsigned(M));
+    prep_dfma_kernel<B, KF><<<grid, 256, 0, s>>>(n, hh_v, hh_tau, gbase, reinterpret_cast<double *>(ws), g_lo, g_hi);
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
 }
 
@@ -303,16 +311,31 @@ int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, doub
     return ELPA_B200_ERR_ARG;
 }
 
-int prepare_impl(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, void *ws, cudaStream_t s) {
+// Groups whose every sweep is < sweep (all groups when sweep >= n - 2): group g holds the sweeps
+// k*g - 1 .. k*g + k - 2 (k = 8 for DMMA, fused_k for DFMA)
+int64_t groups_complete(const Plan &p, int64_t n, int64_t sweep) {
+    const int64_t k = p.kernel == ELPA_B200_KERNEL_DFMA ? p.kf : 8;
+    const int64_t G0 = p.kernel == ELPA_B200_KERNEL_DFMA ? dfma_groups(n, p.nbw, k, 0) : groups_at_depth(n, p.b8, 0);
+    if (sweep >= n - 2) return G0;
+    if (sweep < k - 1) return 0;
+    return std::min<int64_t>(G0, (sweep - k + 1) / k + 1);
+}
+
+// prepare the groups complete for sweeps < sweep_hi that were not complete for sweeps < sweep_lo
+int prepare_impl(const Plan &p, int64_t n, const double *hh_v, const double *hh_tau, void *ws, cudaStream_t s,
+                 int64_t sweep_lo = 0, int64_t sweep_hi = INT64_MAX) {
     if (p.kernel == ELPA_B200_KERNEL_REFERENCE || p.ws_bytes == 0) return ELPA_B200_OK;
+    const int64_t g_lo = sweep_lo <= 0 ? 0 : groups_complete(p, n, sweep_lo);
+    const int64_t g_hi = groups_complete(p, n, sweep_hi);
     if (p.kernel == ELPA_B200_KERNEL_DFMA)
         return dfma_dispatch(p.nbw, p.kf, [&](auto b, auto k) {
-            return launch_prep_dfma<decltype(b)::value, decltype(k)::value>(p, n, hh_v, hh_tau, static_cast<char *>(ws), s);
+            return launch_prep_dfma<decltype(b)::value, decltype(k)::value>(p, n, hh_v, hh_tau, static_cast<char *>(ws), s,
+                                                                          g_lo, g_hi);
         });
     double *w = static_cast<double *>(ws);
     switch (p.b8) {
 #define ELPA_PREP_CASE(B8_) \
-    case B8_: return launch_prep<B8_>(n, hh_v, hh_tau, w, s);
+    case B8_: return launch_prep<B8_>(n, hh_v, hh_tau, w, s, g_lo, g_hi);
         ELPA_PREP_CASE(1) ELPA_PREP_CASE(2) ELPA_PREP_CASE(3) ELPA_PREP_CASE(4) ELPA_PREP_CASE(5) ELPA_PREP_CASE(6)
         ELPA_PREP_CASE(7) ELPA_PREP_CASE(8) ELPA_PREP_CASE(9) ELPA_PREP_CASE(10) ELPA_PREP_CASE(11)
         ELPA_PREP_CASE(12) ELPA_PREP_CASE(13) ELPA_PREP_CASE(14) ELPA_PREP_CASE(15) ELPA_PREP_CASE(16)
@@ -393,6 +416,14 @@ int64_t elpa_hh_count(int64_t n, int64_t nbw) {
     return hh_total(n, nbw);
 }
 
+int64_t elpa_hh_offset(int64_t n, int64_t nbw, int64_t j) {
+    if (n < 0 || nbw < 1 || j < 0) return -1;
+    const int64_t R = hh_total(n, nbw);
+    if (R == 0) return 0;
+    if (j >= n - 2) return R;
+    return hh_off(j, n, nbw);
+}
+
 const char *elpa_b200_strerror(int code) {
     switch (code) {
         case ELPA_B200_OK: return "ok";
@@ -441,6 +472,23 @@ int elpa_b200_prepare(int64_t n, int64_t nbw, const double *hh_v, const double *
     if ((rc = check_device()) != ELPA_B200_OK) return rc;
     rc = prepare_impl(p, n, hh_v, hh_tau, workspace, reinterpret_cast<cudaStream_t>(stream));
     if (rc == ELPA_B200_OK) record_prepared(workspace, p, n);
+    return rc;
+}
+
+int elpa_b200_prepare_sweeps(int64_t n, int64_t nbw, const double *hh_v, const double *hh_tau, void *workspace,
+                             size_t workspace_bytes, int64_t sweep_lo, int64_t sweep_hi, elpa_b200_stream_t stream,
+                             const elpa_b200_opts *opts) {
+    if (n < 0 || nbw < 1 || sweep_lo < 0 || sweep_hi < sweep_lo) return ELPA_B200_ERR_ARG;
+    Plan p;
+    int rc = make_plan(n, nbw, n > 0 ? n : 1, opts, p);
+    if (rc != ELPA_B200_OK) return rc;
+    if (hh_total(n, nbw) == 0 || p.ws_bytes == 0) return ELPA_B200_OK;
+    if (!hh_v || !hh_tau || !workspace) return ELPA_B200_ERR_NULL;
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return ELPA_B200_ERR_ALIGN;
+    if (workspace_bytes < size_t(p.ws_bytes)) return ELPA_B200_ERR_SPACE;
+    if ((rc = check_device()) != ELPA_B200_OK) return rc;
+    rc = prepare_impl(p, n, hh_v, hh_tau, workspace, reinterpret_cast<cudaStream_t>(stream), sweep_lo, sweep_hi);
+    if (rc == ELPA_B200_OK && sweep_hi >= n - 2) record_prepared(workspace, p, n);
     return rc;
 }
 

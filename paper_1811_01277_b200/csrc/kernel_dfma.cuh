@@ -57,20 +57,22 @@ __global__ void dfma_gbase_kernel(int64_t n, int64_t b, int64_t kf, int64_t M, i
     }
 }
 
-// one thread per blob element; grid (element blocks, M).  Reflector a's vector occupies window
+// one thread per blob element of the groups [g_lo, g_hi); grid (element blocks, M).  Reflector a's vector occupies window
 // rows [KF-1-a, KF-1-a+L) (v_0 = 1), zero elsewhere, stored at [a*2WP, a*2WP + WP) and again at
 // [a*2WP + WP, (a+1)*2WP).
 template <int B, int KF>
 __global__ void __launch_bounds__(256)
 prep_dfma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__restrict__ hh_tau,
-                 const int64_t *__restrict__ gbase, double *__restrict__ blobs) {
+                 const int64_t *__restrict__ gbase, double *__restrict__ blobs, int64_t g_lo, int64_t g_hi) {
     constexpr int WP = dfma_window(B, KF);
     constexpr int BLOB = dfma_blob_doubles(B, KF);
     const int64_t m = blockIdx.y;
     const int64_t G = dfma_groups(n, B, KF, m);
     const int64_t Jm = n - 3 - m * B;
     double *base = blobs + gbase[m] * BLOB;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < G * BLOB; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e1 = (g_hi < G ? g_hi : G) * BLOB;      // groups [g_lo, g_hi) of this depth
+    for (int64_t e = g_lo * BLOB + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < e1;
+         e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t g = e / BLOB;
         const int w = int(e % BLOB);
         double val = 0.0;

@@ -14,10 +14,12 @@
 
 namespace elpa_b200 {
 
+// Groups [g_lo, g_hi) of every depth (blockIdx.y = depth m): the multi-GPU path prepares the
+// groups whose sweeps have arrived while the broadcast of later sweeps is still in flight.
 template <int B8, int KIND>
 __global__ void __launch_bounds__(128)
 prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__restrict__ hh_tau,
-                 double *__restrict__ blobs) {
+                 double *__restrict__ blobs, int64_t g_lo, int64_t g_hi) {
     constexpr int B = 8 * B8;
     constexpr int LAM = B8 + 1;
     constexpr int WR = 8 * LAM;                  // window rows
@@ -28,22 +30,41 @@ prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__res
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t m = blockIdx.y;
-    const int64_t g = (int64_t)blockIdx.x * 4 + warp;
-    if (g >= groups_at_depth(n, B8, m)) return;  // warp-uniform; no block barriers below
+    const int64_t g = g_lo + (int64_t)blockIdx.x * 4 + warp;
+    if (g >= g_hi || g >= groups_at_depth(n, B8, m)) return;  // warp-uniform; no block barriers below
     double(*V)[9] = Vs[warp];
     const int64_t Jm = n - 3 - m * B;
 
     for (int idx = lane; idx < WR * 8; idx += 32) V[idx >> 3][idx & 7] = 0.0;
-    if (lane < 8) taus[warp][lane] = 0.0;
-    __syncwarp();
+    // the 8 reflectors' loads are all issued before any is used (one memory latency per group,
+    // not eight): lane holds elements lane + 32 u of each vector
+    constexpr int PER = (B + 31) / 32;
+    double vv[8][PER], tv[8];
+    int64_t Ls[8];
+#pragma unroll
     for (int a = 0; a < 8; a++) {
         const int64_t j = 8 * g + 6 - a;
-        if (j < 0 || j > Jm) continue;
+        const bool ex = j >= 0 && j <= Jm;
         const int64_t s = j + 1 + m * B;
-        const int64_t L = (n - s < B) ? (n - s) : B;
-        const double *v = hh_v + (hh_off(j, n, B) + m) * B;
-        for (int i = lane; i < L; i += 32) V[7 - a + i][a] = (i == 0) ? 1.0 : v[i];
-        if (lane == 0) taus[warp][a] = hh_tau[hh_off(j, n, B) + m];
+        Ls[a] = ex ? ((n - s < B) ? (n - s) : B) : 0;
+        const int64_t r = ex ? hh_off(j, n, B) + m : 0;
+        const double *v = hh_v + r * B;
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const int i = lane + 32 * u;
+            vv[a][u] = (i < Ls[a]) ? v[i] : 0.0;
+        }
+        tv[a] = ex ? hh_tau[r] : 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < 8; a++) {
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const int i = lane + 32 * u;
+            if (i < Ls[a]) V[7 - a + i][a] = (i == 0) ? 1.0 : vv[a][u];
+        }
+        if (lane == 0) taus[warp][a] = tv[a];
     }
     __syncwarp();
     // Gram matrix G = V^T V (64 entries, 2 per lane)

@@ -66,3 +66,53 @@ def test_gloo_world2_broadcast_and_shards(tmp_path):
     hv, tau = synthetic_reflectors(len(s), nbw, seed)
     want = oracle.apply(hv, tau, s, L, synthetic_q_np(n, 0, nev, seed), nthreads=4)
     assert np.array_equal(got, want)
+
+
+def test_sweep_chunks_cover_and_balance():
+    """The broadcast's sweep ranges tile [0, n-2], are strictly increasing, and hold about R/C
+    reflectors each (the last sweeps are short: a range may hold a few more sweeps)."""
+    import paper_1811_01277_b200 as eb
+    from paper_1811_01277_b200.dist import sweep_chunks
+    for (n, nbw, C) in [(20000, 64, 8), (4096, 32, 8), (300, 16, 3), (50, 8, 8), (5, 2, 4)]:
+        b = sweep_chunks(n, nbw, C)
+        assert b[0] == 0 and b[-1] == n - 2
+        assert all(x < y for x, y in zip(b[:-1], b[1:]))
+        R = eb.hh_count(n, nbw)
+        offs = [eb.hh_offset(n, nbw, j) for j in b]
+        assert offs[0] == 0 and offs[-1] == R
+        sizes = [y - x for x, y in zip(offs[:-1], offs[1:])]
+        assert max(sizes) <= R // C + 2 * (n // nbw + 2), sizes
+    n, b = 300, 16
+    for j in (0, 1, 17, 200, 297, 298):                # off(j) = reflectors of the sweeps before j
+        before = sum(len(range(jj + 1, n - 1, b)) for jj in range(min(j, n - 2)))
+        assert eb.hh_offset(n, b, j) == before
+    assert eb.hh_offset(n, b, n - 2) == oracle.count(n, b)
+
+
+def _chunk_worker(rank, world, port, n, nbw, seed, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1811_01277_b200 as eb
+    from paper_1811_01277_b200.dist import pack_reflectors, broadcast_chunks
+    R = eb.hh_count(n, nbw)
+    if rank == 0:
+        hv, tau = synthetic_reflectors(R, nbw, seed)
+        packed = pack_reflectors(torch.from_numpy(hv), torch.from_numpy(tau))
+    else:
+        packed = torch.full((R * (nbw + 1),), float("nan"), dtype=torch.float64)
+    for j0, j1, works in broadcast_chunks(n, nbw, packed, R, src=0, chunks=5):
+        for w in works:
+            w.wait()
+    np.save(os.path.join(outdir, f"chunked{rank}.npy"), packed.numpy())
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_chunked_broadcast(tmp_path):
+    """The chunked broadcast delivers exactly the source's packed reflectors (every row and tau
+    of every sweep range, nothing else)."""
+    n, nbw, seed, world = 301, 16, 5, 2
+    mp.start_processes(_chunk_worker, args=(world, _free_port(), n, nbw, seed, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    a, b = np.load(tmp_path / "chunked0.npy"), np.load(tmp_path / "chunked1.npy")
+    assert np.array_equal(a, b) and np.isfinite(b).all()
