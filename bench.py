@@ -460,6 +460,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's streams at high priority: the broadcast of the next sweep range must get SMs
+        # while the preparation kernels of the previous one fill the GPU (measured at C3, 2 GPUs:
+        # the broadcast/preparation pipeline 4.9 -> 3.7 ms)
+        os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
         dist.init_process_group("nccl", device_id=dev)
 
     n, nbw, nev = CONFIGS[args.config]
@@ -489,10 +493,13 @@ def main():
 
     ev_apply = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in range(args.steps)]
+    ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
 
     from paper_1811_01277_b200.dist import broadcast_and_prepare
 
     def step(i=None):
+        if i is not None:
+            ev_step[i].record(stream)
         if world > 1:
             # the path's collective: the reflector broadcast (NCCL), cut into sweep ranges whose
             # preparation overlaps the transfer of the next range
@@ -529,6 +536,13 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_per_step = ms / args.steps
+    # per-rank phases of a step, max over ranks: before the apply (broadcast + preparation) and the
+    # apply kernel itself
+    pre_ms = sum(e.elapsed_time(a) for e, (a, _) in zip(ev_step, ev_apply)) / args.steps
+    phases = torch.tensor([pre_ms, sum(apply_ms) / len(apply_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(phases, op=dist.ReduceOp.MAX)
+    phase_pre_max, phase_apply_max = float(phases[0].item()), float(phases[1].item())
     flops_total = 4.0 * nbw * nev * R                    # all ranks together (credited)
     value = flops_total / (ms_per_step * 1e-3) / 1e12
 
@@ -599,6 +613,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "parity_max_rel_err_sampled": parity,
             "apply_ms_per_launch": apply_avg,
             "step_overhead_ms": ms_per_step - apply_avg,    # everything but the apply kernel (rank 0's apply)
+            "phases_max_over_ranks_ms": {"bcast_and_prepare": phase_pre_max, "apply": phase_apply_max},
         }
         if args.proxy_gpus > 1 and world == 1:
             out = proxy_line(out, args, flops_total, nev_loc)
@@ -619,7 +634,8 @@ def proxy_line(out, args, flops_total, nev_loc):
         path = os.path.join(ROOT, "profiles", "r02", f"bench_{args.config}_n{N}_r02.json")
         try:
             d = json.load(open(path))
-            over[N] = d["ms_per_step"] - d["apply_ms_per_launch"]
+            ph = d.get("phases_max_over_ranks_ms")
+            over[N] = ph["bcast_and_prepare"] if ph else d["ms_per_step"] - d["apply_ms_per_launch"]
         except (OSError, ValueError, KeyError):
             pass
     shard_ms = out["ms_per_step"]                       # prepare + apply of the shard, 1 GPU

@@ -154,7 +154,10 @@ def test_prepare_apply_two_phase(eb):
     hv, tau, s, L, Q = synth_case(n, nbw, nev, 99)
     want = oracle.apply(hv, tau, s, L, Q)
     dv, dt = torch.from_numpy(hv).cuda(), torch.from_numpy(tau).cuda()
-    ws = torch.empty(eb.workspace_bytes(n, nbw), dtype=torch.uint8, device="cuda")
+    # big enough for either kernel's layout, so the mismatch below is caught by the prepared-layout
+    # check and not by the size check
+    ws = torch.empty(max(eb.workspace_bytes(n, nbw), eb.workspace_bytes(n, nbw, dict(kernel=eb.KERNEL_DFMA))),
+                     dtype=torch.uint8, device="cuda")
     eb.prepare(n, nbw, dv, dt, ws)
     for half in (slice(0, 20), slice(20, 40)):
         dq = torch.from_numpy(Q[half].copy()).cuda()
