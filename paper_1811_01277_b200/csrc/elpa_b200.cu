@@ -103,7 +103,6 @@ int64_t dfma_total_groups(int64_t n, int64_t nbw, int kf) {
 // other's per-step barriers; work items (tile group, depth pass) are spread dynamically over
 // all SMs, so balance no longer depends on nev / (8 * #SMs).
 void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int &K) {
-    (void)ntile; (void)M;
     K = 1;
     // best of 5 per shape (profiles/shape_sweep_r01_final2.jsonl), TF/s:
     //                 C2    C4    C3/8  C3/4  C3    C5/8
@@ -111,7 +110,13 @@ void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int
     //   (2,2,2,1)   19.4  25.7  26.6  27.4  27.7  27.5
     // MEDIUM autotuning with the final kernel (profiles/autotune_medium_r01_final.jsonl): C3 keeps
     // (1,2,4,1) 28.7, C4 keeps (2,2,2,1) 26.1, C2 (nbw = 32) prefers (4,2,2,1) 22.3 over 21.2
+    // Round 2 (profiles/r02/thin_shard_shapes_r02.jsonl, the 2000 - 5000-column shards of n = 20000
+    // at publish periods 8/16/32): one depth warp with two 2-tile column warps beats (2,2,2,1) by
+    // 3-4% (26.6 vs 25.7 TF/s at 2000 columns, 27.0 vs 25.9 at 2500); the n = 60000 shard (938
+    // depth passes) prefers four column warps, (1,4,2,1) 27.2 TF/s.
     if (b8 == 8 && ntile >= 2000) { D = 1; CW = 2; NCT = 4; }
+    else if (b8 == 8 && M > 600) { D = 1; CW = 4; NCT = 2; }
+    else if (b8 == 8) { D = 1; CW = 2; NCT = 2; }
     else if (b8 == 4 && ntile < 2000) { D = 4; CW = 2; NCT = 2; }
     else { D = 2; CW = 2; NCT = 2; }   // also the default of the small menu (nbw != 8/16/32/64)
 }
@@ -289,7 +294,7 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     if (rc == ELPA_B200_OK) {
         apply_dmma_kernel<KIND, B8, D, CW, NCT, K><<<unsigned(grid), DmmaCfg<KIND, B8, D, CW, NCT, K>::THREADS,
                                                      DmmaCfg<KIND, B8, D, CW, NCT, K>::SMEM, s>>>(n, nev, ws, Q, ldq, prog,
-                                                                                                  pub_period());
+                                                                                                  pub_period((nev + 7) / 8));
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     }
     if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;

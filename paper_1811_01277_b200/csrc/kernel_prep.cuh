@@ -67,12 +67,23 @@ prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__res
         if (lane == 0) taus[warp][a] = tv[a];
     }
     __syncwarp();
-    // Gram matrix G = V^T V (64 entries, 2 per lane)
-    for (int e = lane; e < 64; e += 32) {
-        const int a = e >> 3, l = e & 7;
-        double acc = 0.0;
-        for (int w = 0; w < WR; w++) acc = fma(V[w][a], V[w][l], acc);
-        Gs[warp][a][l] = acc;
+    // Gram matrix G = V^T V on the FP64 tensor cores: 9 chunks x 2 DMMA.8x8x4 (K = window rows,
+    // k-pair permuted as in the apply kernel).  Lane (g = lane/4, q = lane%4) supplies rows 2q, 2q+1
+    // of the chunk in column g for both operands (A = V^T, B = V hold the same values) and receives
+    // G[g][2q], G[g][2q+1].
+    const int kq = lane & 3, gq = lane >> 2;
+    {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < LAM; i++) {
+            const double x0 = V[8 * i + 2 * kq][gq], x1 = V[8 * i + 2 * kq + 1][gq];
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc.x), "+d"(acc.y) : "d"(x0), "d"(x0));
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc.x), "+d"(acc.y) : "d"(x1), "d"(x1));
+        }
+        Gs[warp][gq][2 * kq] = acc.x;
+        Gs[warp][gq][2 * kq + 1] = acc.y;
     }
     if (lane < 64 / 2) { Ts[warp][lane >> 3][lane & 7] = 0.0; Ts[warp][(lane + 32) >> 3][(lane + 32) & 7] = 0.0; }
     __syncwarp();
@@ -90,20 +101,21 @@ prep_dmma_kernel(int64_t n, const double *__restrict__ hh_v, const double *__res
         __syncwarp();
     }
     double *blob = blobs + (group_base(n, B8, m) + g) * blob_doubles(LAM, KIND);
-    // U = -V T (window rows x 8): the dot phase then yields W^T = Q_W^T U directly
-    // (W = -T^T V^T Q_W), so the apply kernel needs no separate T step
-    auto U = [&](int w, int a) {
-        double acc = 0.0;
-        for (int p = 0; p <= a; p++) acc = fma(V[w][p], Ts[warp][p][a], acc);
-        return -acc;
-    };
-    const int kq = lane & 3, gq = lane >> 2;
+    // U^T = -T^T V^T on the tensor cores (M = reflector a, N = window rows in 9 tiles, K = 8
+    // reflectors in 2 k-steps): the accumulator of tile i is (U[8i+2q][g], U[8i+2q+1][g]) — the dot
+    // B-fragment layout of the apply kernel — and the B operand (V[8i+g][2q], V[8i+g][2q+1]) is the
+    // update B-fragment.  (U = -V T: the dot phase then yields W^T = Q_W^T U directly, so the apply
+    // kernel needs no separate T step.)
+    const double ta0 = -Ts[warp][2 * kq][gq], ta1 = -Ts[warp][2 * kq + 1][gq];
+#pragma unroll
     for (int i = 0; i < LAM; i++) {
-        double2 d, u;
-        d.x = U(8 * i + 2 * kq, gq);
-        d.y = U(8 * i + 2 * kq + 1, gq);
+        double2 d = make_double2(0.0, 0.0), u;
         u.x = V[8 * i + gq][2 * kq];
         u.y = V[8 * i + gq][2 * kq + 1];
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(d.x), "+d"(d.y) : "d"(ta0), "d"(u.x));
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(d.x), "+d"(d.y) : "d"(ta1), "d"(u.y));
         reinterpret_cast<double2 *>(blob)[i * 32 + lane] = d;
         reinterpret_cast<double2 *>(blob + 64 * LAM)[i * 32 + lane] = u;
     }
