@@ -34,7 +34,7 @@ UNIT = "TFLOP/s"
 CFG_INDEX = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
 PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.jsonl")
 PEAKS32_FILE = os.path.join(ROOT, "profiles", "fp32_peaks_r01.jsonl")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02", "ncu_summary_r02.json")
 
 
 def parse():
@@ -588,13 +588,15 @@ def main():
     try:
         summ = json.load(open(NCU_SUMMARY))
         key = f"{args.config}:{world}"
-        if key in summ:
-            traffic = summ[key].get("dram_bytes_per_launch")
+        kname = "apply_dmma_kwin_kernel" if " K=1 " not in desc else "apply_dmma_kernel"
+        if key in summ and kname + "<" in summ[key].get("kernel", ""):
+            traffic = summ[key].get("dram_bytes_per_launch")   # only for the kernel it was captured on
     except (OSError, ValueError):
         pass
     roofline = {"bound": "tensor" if args.kernel == "dmma" else "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic if args.kernel == "dmma" else None,
-                "kernel": "apply_dmma_kernel" if args.kernel == "dmma" else "apply_dfma_kernel",
+                "kernel": ("apply_dfma_kernel" if args.kernel == "dfma" else
+                           "apply_dmma_kwin_kernel" if " K=1 " not in desc else "apply_dmma_kernel"),
                 "peak_source": ("measured FP64 DMMA m8n8k4 peak" if args.kernel == "dmma" else "measured FP64 DFMA peak")
                                + " on this pool's B200 (profiles/fp64_peaks_r01.jsonl)",
                 "apply_ms": apply_avg,

@@ -18,6 +18,7 @@
 #include "kernel_dmma.cuh"
 #include "kernel_prep.cuh"
 #include "kernel_dfma.cuh"
+#include "kernel_dmma_kwin.cuh"
 #include "kernel_reference.cuh"
 
 #include <mutex>
@@ -67,6 +68,18 @@ bool dfma_compiled(int64_t nbw, int kf, int CW) {
 #define ELPA_SMALL_SHAPES(X) X(2, 2, 2, 1) X(1, 2, 2, 1)
 constexpr Shape kSmallShapes[] = {ELPA_SMALL_SHAPES(ELPA_SHAPE_ENTRY)};
 
+// One depth per item and K >= 2 groups per step in one register window (kernel_dmma_kwin.cuh),
+// compiled for nbw = 32 and 64: (1, CW, NCT, K)
+#define ELPA_KWIN_SHAPES(X) X(1, 2, 2, 2) X(1, 4, 2, 2) X(1, 4, 1, 4) X(1, 4, 1, 2) X(1, 6, 2, 2) X(1, 8, 2, 2) \
+    X(1, 3, 2, 2) X(1, 4, 2, 3) X(1, 8, 1, 2)
+constexpr Shape kKwinShapes[] = {ELPA_KWIN_SHAPES(ELPA_SHAPE_ENTRY)};
+bool kwin_compiled(int b8, int D, int CW, int NCT, int K) {
+    if (b8 != 4 && b8 != 8) return false;
+    for (const Shape &s : kKwinShapes)
+        if (s.D == D && s.CW == CW && s.NCT == NCT && s.K == K) return true;
+    return false;
+}
+
 bool shape_compiled(int D, int CW, int NCT, int K);
 bool shape_compiled(int D, int CW, int NCT, int K, int b8) {
     if (!b8_full_menu(b8)) {
@@ -110,11 +123,14 @@ void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int
     //   (2,2,2,1)   19.4  25.7  26.6  27.4  27.7  27.5
     // MEDIUM autotuning with the final kernel (profiles/autotune_medium_r01_final.jsonl): C3 keeps
     // (1,2,4,1) 28.7, C4 keeps (2,2,2,1) 26.1, C2 (nbw = 32) prefers (4,2,2,1) 22.3 over 21.2
-    // Round 2 (profiles/r02/thin_shard_shapes_r02.jsonl, the 2000 - 5000-column shards of n = 20000
+    // Round 2: wide stripes run the two-group register window (kernel_dmma_kwin.cuh) with four
+    // column warps of two tiles: 29.6 vs 28.95 TF/s for (1,2,4,1) at C3
+    // (profiles/r02/kwin_shapes_r02.jsonl).  Thin stripes
+    // (profiles/r02/thin_shard_shapes_r02.jsonl, the 2000 - 5000-column shards of n = 20000
     // at publish periods 8/16/32): one depth warp with two 2-tile column warps beats (2,2,2,1) by
     // 3-4% (26.6 vs 25.7 TF/s at 2000 columns, 27.0 vs 25.9 at 2500); the n = 60000 shard (938
     // depth passes) prefers four column warps, (1,4,2,1) 27.2 TF/s.
-    if (b8 == 8 && ntile >= 2000) { D = 1; CW = 2; NCT = 4; }
+    if (b8 == 8 && ntile >= 2000) { D = 1; CW = 4; NCT = 2; K = 2; }   // kernel_dmma_kwin.cuh
     else if (b8 == 8 && M > 600) { D = 1; CW = 4; NCT = 2; }
     else if (b8 == 8) { D = 1; CW = 2; NCT = 2; }
     else if (b8 == 4 && ntile < 2000) { D = 4; CW = 2; NCT = 2; }
@@ -167,7 +183,8 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
         if (K == 0) K = Ka;
     }
     if (K == 0) K = 1;
-    if (!shape_compiled(D, CW, NCT, K, p.b8)) return ELPA_B200_ERR_ARG;
+    const bool kwin = K >= 2 && kwin_compiled(p.b8, D, CW, NCT, K);
+    if (!kwin && !shape_compiled(D, CW, NCT, K, p.b8)) return ELPA_B200_ERR_ARG;
     p.D = D; p.CW = CW; p.NCT = NCT; p.K = K;
     p.grid_req = o ? o->grid_ctas : 0;
     if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
@@ -175,7 +192,8 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     p.items = p.nx * ((M + D - 1) / D);
     p.grid = p.items;          // capped by co-residency at launch
     p.threads = 32 * D * CW;
-    p.smem = dmma_smem(p.b8, D, CW, NCT, K);
+    p.smem = kwin ? size_t(2) * K * blob_doubles(p.b8 + 1, 0) * 8 + size_t(2) * K * CW * NCT * 64 * 8 + 2 * 2 * 8 + 16
+                  : dmma_smem(p.b8, D, CW, NCT, K);
     if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;   // shape does not fit this nbw
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1, 0) * 8 : 0;
     return ELPA_B200_OK;
@@ -301,9 +319,42 @@ int launch_dmma_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     return rc;
 }
 
+template <int B8, int CW, int NCT, int K>
+int launch_kwin_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq, cudaStream_t s) {
+    using Cfg = KwinCfg<B8, CW, NCT, K>;
+    auto kern = apply_dmma_kwin_kernel<B8, CW, NCT, K>;
+    int per_sm = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS, Cfg::SMEM) != cudaSuccess ||
+        per_sm < 1)
+        return fail_cuda();
+    int64_t grid = int64_t(per_sm) * sm_count();
+    if (p.grid_req > 0 && p.grid_req < grid) grid = p.grid_req;
+    if (grid > p.items) grid = p.items;
+    uint64_t *prog = nullptr;
+    const size_t pbytes = size_t(p.items + 1) * 8;
+    if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
+    int rc = cudaMemsetAsync(prog, 0, pbytes, s) == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+    if (rc == ELPA_B200_OK) {
+        kern<<<unsigned(grid), Cfg::THREADS, Cfg::SMEM, s>>>(n, nev, ws, Q, ldq, prog, pub_period((nev + 7) / 8));
+        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    }
+    if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    return rc;
+}
+
 template <int B8>
 int launch_dmma_b8(const Plan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq,
                    cudaStream_t s) {
+    if constexpr (B8 == 4 || B8 == 8) {
+#define ELPA_KWIN(D_, CW_, NCT_, K_)                            \
+        if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
+            return launch_kwin_shape<B8, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
+        if (p.K >= 2) {
+            ELPA_KWIN_SHAPES(ELPA_KWIN)
+        }
+#undef ELPA_KWIN
+    }
 #define ELPA_SHAPE(D_, CW_, NCT_, K_)                          \
     if (p.D == D_ && p.CW == CW_ && p.NCT == NCT_ && p.K == K_) \
         return launch_dmma_shape<KIND_DMMA, B8, D_, CW_, NCT_, K_>(p, n, nev, ws, Q, ldq, s);
