@@ -21,6 +21,8 @@ CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-
 # ELPA_B200_DEBUG=1: debug build with the kernels' wait watchdog (trap after ~10 s of wall time)
 if os.environ.get("ELPA_B200_DEBUG") == "1":
     CFLAGS += ["-DELPA_B200_WATCHDOG"]
+# development A/B builds only (tools/ab_run.sh): extra preprocessor flags, e.g. "-DKWIN_ABL=1"
+CFLAGS += os.environ.get("ELPA_B200_DEV_CFLAGS", "").split()
 LFLAGS = ARCH + ["-shared", "-cudart", "static"]
 
 

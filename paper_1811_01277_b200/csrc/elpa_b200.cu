@@ -192,8 +192,7 @@ int make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, Plan
     p.items = p.nx * ((M + D - 1) / D);
     p.grid = p.items;          // capped by co-residency at launch
     p.threads = 32 * D * CW;
-    p.smem = kwin ? size_t(2) * K * blob_doubles(p.b8 + 1, 0) * 8 + size_t(2) * K * CW * NCT * 64 * 8 + 2 * 2 * 8 + 16
-                  : dmma_smem(p.b8, D, CW, NCT, K);
+    p.smem = kwin ? kwin_smem(p.b8, CW, NCT, K, kwin_stages(p.b8, CW, NCT, K)) : dmma_smem(p.b8, D, CW, NCT, K);
     if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;   // shape does not fit this nbw
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1, 0) * 8 : 0;
     return ELPA_B200_OK;
@@ -249,7 +248,7 @@ int launch_dfma(const Plan &p, int64_t n, int64_t nev, const char *ws, double *Q
     if (p.grid_req > 0 && p.grid_req < grid) grid = p.grid_req;
     if (grid > p.items) grid = p.items;
     uint64_t *prog = nullptr;
-    const size_t pbytes = size_t(p.items + 1) * 8;
+    const size_t pbytes = size_t(p.items * CW + 1) * 8;   // one word per (item, column warp) + counter
     if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
     int rc = cudaMemsetAsync(prog, 0, pbytes, s) == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
@@ -332,7 +331,7 @@ int launch_kwin_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     if (p.grid_req > 0 && p.grid_req < grid) grid = p.grid_req;
     if (grid > p.items) grid = p.items;
     uint64_t *prog = nullptr;
-    const size_t pbytes = size_t(p.items + 1) * 8;
+    const size_t pbytes = size_t(p.items * CW + 1) * 8;   // one word per (item, column warp) + counter
     if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
     int rc = cudaMemsetAsync(prog, 0, pbytes, s) == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {

@@ -11,11 +11,34 @@
 // the step the bottom K chunks (T(st) + W-K ..) are final for depth m and go back to HBM, and the
 // K chunks T(st+1) .. T(st+1) + K-1, prefetched with cp.async one step ahead, enter at the top.
 // Work items, dequeue, the fragment ring (consumed mbarriers, no CTA barrier per step) and the
-// progress words are those of kernel_dmma.cuh with D = 1.
+// progress words are those of kernel_dmma.cuh with D = 1, except that the words
+// are per column warp (no CTA barrier on publish steps).
 #pragma once
 #include "kernel_dmma.cuh"
 
+#ifndef KWIN_ABL
+#define KWIN_ABL 0      // development ablation mask (wrong results; timing only): 0 in the product
+#endif
+
 namespace elpa_b200 {
+
+// Shared-memory and occupancy arithmetic of the kernel, also used by the host plan (make_plan).
+constexpr int kwin_reg_est(int b8, int NCT, int K) { return 4 * (b8 + K) * NCT + 90; }   // W = b8 + K
+constexpr int kwin_minb(int b8, int CW, int NCT, int K) {
+    const int r = 65536 / (32 * CW * kwin_reg_est(b8, NCT, K));
+    return r < 1 ? 1 : (r > 8 ? 8 : r);
+}
+constexpr size_t kwin_smem(int b8, int CW, int NCT, int K, int stages) {
+    return size_t(stages) * K * 128 * (b8 + 1) * 8          // fragment ring: stages x K blobs
+           + size_t(2) * K * CW * NCT * 64 * 8               // Q intake, double-buffered
+           + size_t(2) * stages * 8 + 16;                    // mbarriers + item slot
+}
+// Fragment ring depth: 3 stages where they fit the register-limited CTA count (228 KB per SM, 1 KB
+// reserved per CTA), else 2.  Measured at C3 (1,4,2,2): 2 -> 3 stages 30.42 -> 30.60 TF/s; a
+// shape that would lose a CTA per SM keeps 2 ((1,2,2,2): 28.4 -> 23.7 with 3).
+constexpr int kwin_stages(int b8, int CW, int NCT, int K) {
+    return size_t(kwin_minb(b8, CW, NCT, K)) * (kwin_smem(b8, CW, NCT, K, 3) + 1024) <= size_t(233472) ? 3 : 2;
+}
 
 // compile-time loop: f(integral_constant<int, I>) for I = I0 .. I1-1
 template <int I0, int I1, class F>
@@ -33,16 +56,11 @@ struct KwinCfg {
     static constexpr int BLOB = 128 * LAM;                // doubles per prepared group (DMMA layout)
     static constexpr int THREADS = 32 * CW;
     static constexpr int T = CW * NCT;                    // 8-column tiles per work item
-    // fragment stages of K blobs each: 2 (issued one step ahead: a step of K groups hides the copy;
-    // 4 stages of K blobs would cost 147 KB of shared memory at K = 4 and one CTA per SM)
-    // (3 stages measured slower: (1,2,2,2) 27.1 -> 21.3 TF/s at C3, one CTA fewer per SM)
-    static constexpr int STAGES = 2;
+    static constexpr int STAGES = kwin_stages(B8, CW, NCT, K);   // fragment ring (K blobs per stage)
     static constexpr size_t SMEM_BLOBS = size_t(STAGES) * K * BLOB * sizeof(double);
     static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
-    static constexpr size_t SMEM = SMEM_BLOBS + SMEM_INTAKE + 2 * STAGES * 8 + 16;
-    static constexpr int REG_EST = 4 * W * NCT + 90;
-    static constexpr int MINB_RAW = 65536 / (THREADS * REG_EST);
-    static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW > 8 ? 8 : MINB_RAW);
+    static constexpr size_t SMEM = kwin_smem(B8, CW, NCT, K, STAGES);
+    static constexpr int MINB = kwin_minb(B8, CW, NCT, K);
 };
 
 // One compact-WY group (DmmaGroup's arithmetic) on window chunks [OFF, OFF + LAM) of q[NCT][W].
@@ -125,11 +143,15 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
 
     for (;;) {
         if (threadIdx.x == 0)
-            *s_item = int(atomicAdd(reinterpret_cast<unsigned long long *>(prog + int64_t(NX) * M), 1ull));
+            *s_item = int(atomicAdd(reinterpret_cast<unsigned long long *>(prog + int64_t(NX) * M * CW), 1ull));
         __syncthreads();
         const int k = *s_item;
         if (k >= NX * M) break;
         const int p = k / NX, x = k % NX;                  // depth p, tile group x
+        // progress word of this warp's columns in item k: column warp cw of item (x, p + 1) reads
+        // exactly the columns column warp cw of item (x, p) writes, so each warp publishes its own
+        // word (release after its lanes' fences) and waits on its producer warp's word only
+        uint64_t *wprog = prog + int64_t(k) * CW + cw;
         const int tile_end = min(ntile, (x + 1) * T);
         double *qcol[NCT];
         uint32_t okmask = 0;
@@ -169,15 +191,15 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
 
         uint32_t seen = 0;
         auto await_chunk = [&](int c) {                    // chunk c final from depth p-1
-            if (p == 0 || c < 0) return;
+            if (p == 0 || c < 0 || (KWIN_ABL & 8)) return;
             const uint32_t need = uint32_t(C0 + 2 - c);
             if (seen >= need) return;
             if (lane == 0) {
-                uint64_t v = ld_acquire_u64(prog + (k - NX));
+                uint64_t v = ld_acquire_u64(wprog - int64_t(NX) * CW);
                 ELPA_WATCHDOG_START();
                 while (v < need) {
                     __nanosleep(128);
-                    v = ld_acquire_u64(prog + (k - NX));
+                    v = ld_acquire_u64(wprog - int64_t(NX) * CW);
                     ELPA_WATCHDOG_CHECK();
                 }
                 seen = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(v);
@@ -188,6 +210,7 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
         auto intake = [&](int st) {
             const int top = C0 - (st + 1) * K - (K - 1);
             await_chunk(top);
+            if (KWIN_ABL & 2) { cp_async_commit(); return; }
 #pragma unroll
             for (int j = 0; j < K; j++) {
                 const int c = top + j;
@@ -229,10 +252,17 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
             const int gs = gstep0 + st, stage = gs % S;
             mbar_wait(&bars[stage], uint32_t((gs / S) & 1));
             const double *sb = sblob + stage * K * BLOB;
-            static_for_kwin<0, K>([&](auto jc) {
-                constexpr int j = decltype(jc)::value;
-                if (st * K + j < NT) dmma_group_at<LAM, NCT, W, K - 1 - j>(q, sb + j * BLOB, lane);
-            });
+            if (st * K + K <= NT) {                        // a full step: one basic block, so the
+                static_for_kwin<0, K>([&](auto jc) {       // groups' DMMAs interleave (+1.7% at C3)
+                    constexpr int j = decltype(jc)::value;
+                    dmma_group_at<LAM, NCT, W, K - 1 - j>(q, sb + j * BLOB, lane);
+                });
+            } else {                                       // the item's last step, NT % K groups
+                static_for_kwin<0, K>([&](auto jc) {
+                    constexpr int j = decltype(jc)::value;
+                    if (st * K + j < NT) dmma_group_at<LAM, NCT, W, K - 1 - j>(q, sb + j * BLOB, lane);
+                });
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&ebars[stage]);     // this warp is done with the stage
             if (st + 1 >= nsteps) break;                   // the final window is written back below
@@ -243,22 +273,24 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
                 double2 bot[NCT];
 #pragma unroll
                 for (int t = 0; t < NCT; t++) bot[t] = q[t][W - K + jj];
-                store_tiles(bot, 8 * (tst + W - K + jj) + rsub);
+                if (!(KWIN_ABL & 1)) store_tiles(bot, 8 * (tst + W - K + jj) + rsub);
             }
-            const bool pub = pub_step(st);
-            if (pub) __threadfence();
+            const bool pub = (KWIN_ABL & 32) ? false : pub_step(st);
+            if (pub) __threadfence();                      // this lane's stores, before the warp's release
             // slide by K chunks; the new top chunks arrived during this step
             if (st + 1 < nsteps - 1) cp_async_wait<1>(); else cp_async_wait<0>();
 #pragma unroll
             for (int t = 0; t < NCT; t++) {
+                if (!(KWIN_ABL & 16)) {
 #pragma unroll
-                for (int i = W - 1; i >= K; i--) q[t][i] = q[t][i - K];
+                    for (int i = W - 1; i >= K; i--) q[t][i] = q[t][i - K];
+                }
 #pragma unroll
                 for (int j = 0; j < K; j++) q[t][j] = sintake[islot(st & 1, j, t)];
             }
-            if (pub) {
-                __syncthreads();
-                if (threadIdx.x == 0) st_release_u64(prog + k, uint64_t(C0 + 2 - (tst + W - K)));
+            if (pub) {                                     // per-warp word: no CTA barrier
+                __syncwarp();
+                if (lane == 0) st_release_u64(wprog, uint64_t(C0 + 2 - (tst + W - K)));
             }
             pub_count = pub ? 0 : pub_count + 1;
         }
@@ -273,8 +305,9 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
             store_tiles(col, 8 * (tf + i) + rsub);
         }
         __threadfence();
-        __syncthreads();                                   // item complete
-        if (threadIdx.x == 0) st_release_u64(prog + k, kPassDone);
+        __syncwarp();
+        if (lane == 0) st_release_u64(wprog, kPassDone);  // this warp's columns of the pass are final
+        __syncthreads();                                   // s_item is rewritten by the next dequeue
         gstep0 += nsteps;
     }
 }

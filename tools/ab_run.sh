@@ -7,7 +7,7 @@ out=$1; shift; shapes=$1; shift
 lib=paper_1811_01277_b200/libelpa_b200.so
 cp $lib tools/ab/lib_orig.so
 for round in 1 2; do
-  for v in A B; do
+  for v in ${VARIANTS:-A B}; do
     cp tools/ab/lib$v.so $lib
     SHAPES="$shapes" REPS=${REPS:-5} timeout 600 python ${TOOL:-tools/quick_perf.py} "$@" | sed "s/^{/{\"lib\": \"$v\", \"round\": $round, /" >> $out
   done
