@@ -51,8 +51,9 @@ bool b8_supported(int64_t nbw) { return nbw % 8 == 0 && nbw >= 8 && nbw <= 128; 
 // (D, CW, NCT) menu of compiled DMMA configurations
 // (D depth warps, CW column warps, NCT tiles per warp, K groups per step)
 struct Shape { int D, CW, NCT, K; };
-// K = 1 throughout: measured faster than K = 2/4 at every config (profiles/shape_sweep_r01_k.jsonl);
-// the kernel keeps K as a template parameter for later work.
+// K = 1 throughout for apply_dmma_kernel (its K = 2/4 variants were slower at every config,
+// profiles/shape_sweep_r01_k.jsonl); groups_per_step K >= 2 selects the register-window kernel
+// (kernel_dmma_kwin.cuh, kKwinShapes below).
 #define ELPA_SHAPES(X) X(1, 2, 4, 1) X(2, 2, 4, 1) X(4, 2, 4, 1) X(8, 1, 4, 1) X(2, 4, 2, 1) X(2, 2, 3, 1) \
     X(2, 2, 2, 1) X(4, 4, 2, 1) X(2, 4, 3, 1) X(2, 1, 2, 1) X(1, 2, 2, 1) X(4, 2, 2, 1) X(2, 1, 4, 1) \
     X(1, 1, 4, 1) X(1, 1, 2, 1) X(1, 4, 2, 1) X(2, 1, 3, 1)
@@ -123,16 +124,16 @@ void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int
     //   (2,2,2,1)   19.4  25.7  26.6  27.4  27.7  27.5
     // MEDIUM autotuning with the final kernel (profiles/autotune_medium_r01_final.jsonl): C3 keeps
     // (1,2,4,1) 28.7, C4 keeps (2,2,2,1) 26.1, C2 (nbw = 32) prefers (4,2,2,1) 22.3 over 21.2
-    // Round 2: wide stripes run the two-group register window (kernel_dmma_kwin.cuh) with four
-    // column warps of two tiles: 29.6 vs 28.95 TF/s for (1,2,4,1) at C3
-    // (profiles/r02/kwin_shapes_r02.jsonl).  Thin stripes
-    // (profiles/r02/thin_shard_shapes_r02.jsonl, the 2000 - 5000-column shards of n = 20000
-    // at publish periods 8/16/32): one depth warp with two 2-tile column warps beats (2,2,2,1) by
-    // 3-4% (26.6 vs 25.7 TF/s at 2000 columns, 27.0 vs 25.9 at 2500); the n = 60000 shard (938
-    // depth passes) prefers four column warps, (1,4,2,1) 27.2 TF/s.
-    if (b8 == 8 && ntile >= 2000) { D = 1; CW = 4; NCT = 2; K = 2; }   // kernel_dmma_kwin.cuh
-    else if (b8 == 8 && M > 600) { D = 1; CW = 4; NCT = 2; }
-    else if (b8 == 8) { D = 1; CW = 2; NCT = 2; }
+    // Round 2: nbw = 64 runs the two-group register window (kernel_dmma_kwin.cuh) everywhere
+    // (profiles/r02/kwin_final_shapes_r02.jsonl, TF/s):
+    //   columns (n = 20000)  500   1000  2000  2500  5000  10000 20000 | n = 60000: 3750  7500
+    //   (1,4,2,2) K=2       14.2  22.7  26.7  27.1  29.0  29.9  30.6  |            28.4  29.0
+    //   (1,4,1,2) K=2       21.6  24.7  26.5  26.6  27.2  27.3        |            26.4  26.5
+    //   round 1's K = 1     19.7  24.3  26.7  27.0  28.1  28.6  29.0  |            27.4  27.9
+    // Below 250 tiles the one-tile warps win (the wider items leave too few of them per SM).
+    (void)M;
+    if (b8 == 8 && ntile >= 250) { D = 1; CW = 4; NCT = 2; K = 2; }
+    else if (b8 == 8) { D = 1; CW = 4; NCT = 1; K = 2; }
     else if (b8 == 4 && ntile < 2000) { D = 4; CW = 2; NCT = 2; }
     else { D = 2; CW = 2; NCT = 2; }   // also the default of the small menu (nbw != 8/16/32/64)
 }
@@ -335,7 +336,7 @@ int launch_kwin_shape(const Plan &p, int64_t n, int64_t nev, const double *ws, d
     if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
     int rc = cudaMemsetAsync(prog, 0, pbytes, s) == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
     if (rc == ELPA_B200_OK) {
-        kern<<<unsigned(grid), Cfg::THREADS, Cfg::SMEM, s>>>(n, nev, ws, Q, ldq, prog, pub_period((nev + 7) / 8));
+        kern<<<unsigned(grid), Cfg::THREADS, Cfg::SMEM, s>>>(n, nev, ws, Q, ldq, prog, kwin_pub_period((nev + 7) / 8));
         if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
     }
     if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
@@ -806,6 +807,12 @@ std::vector<elpa_b200_opts> autotune_candidates(int64_t n, int64_t nbw, int64_t 
         };
         if (b8_full_menu(b8)) {
             add(kShapes, sizeof(kShapes) / sizeof(kShapes[0]), ELPA_B200_KERNEL_DMMA);
+            for (const Shape &sh : kKwinShapes) {          // the K-group register-window kernel
+                elpa_b200_opts o = mk(ELPA_B200_KERNEL_DMMA, sh.D, sh.CW, sh.NCT);
+                o.groups_per_step = sh.K;
+                Plan p;
+                if (make_plan(n, nbw, nev, &o, p) == ELPA_B200_OK) c.push_back(o);
+            }
             for (int kf : {2, 4, 6}) {                  // the DFMA kernel's fused-reflector count
                 elpa_b200_opts o = mk(ELPA_B200_KERNEL_DFMA, 0, 0, 0);
                 o.fused_k = kf;

@@ -44,6 +44,15 @@ inline int pub_period(int64_t ntile = 1 << 30) {
     return ntile < 2000 ? 16 : 32;
 }
 
+// The register-window kernel (K groups per step) measured its own optimum
+// (profiles/r02/kwin_pub_period_r02.jsonl, profiles/r02/kwin_thin_pub_r02.jsonl): 32 steps for wide
+// stripes, 16 from 400 tiles, 8 below (2500 columns: 27.43 TF/s at 8 against 27.18 at 16).
+inline int kwin_pub_period(int64_t ntile) {
+    const int v = pub_period();
+    if (v != 32) return v;                      // ELPA_B200_PUB override
+    return ntile < 400 ? 8 : (ntile < 2000 ? 16 : 32);
+}
+
 inline int smem_optin() {
     int dev = 0, v = 232448;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);

@@ -11,11 +11,13 @@ def test_levels_and_candidates():
     nf, nm = fast.progress()[1], med.progress()[1]
     assert nf == 2                                      # DMMA + DFMA (reference too slow at C3)
     assert nm > nf + 10                                 # + every compiled (D, CW, NCT) shape
-    kinds = set()
+    kinds, ks = set(), set()
     while (o := med.step()) is not None:
         kinds.add(o["kernel"])
+        ks.add(o["groups_per_step"])
         med.report(1.0)
     assert kinds == {eb.KERNEL_DMMA, eb.KERNEL_DFMA}
+    assert {1, 2} <= ks                                 # the register-window kernel's shapes too
     small = eb.Autotuner(300, 16, 40, eb.AUTOTUNE_FAST)
     assert small.progress()[1] == 3                     # the reference kernel joins for small problems
     odd = eb.Autotuner(300, 6, 40, eb.AUTOTUNE_MEDIUM)
