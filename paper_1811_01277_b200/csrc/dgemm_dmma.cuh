@@ -103,7 +103,7 @@ template <class G, bool BETA>
 __global__ void __launch_bounds__(G::THREADS, G::MINB)
 dgemm_tn_kernel(int M, int N, int K, int k_per_split, double alpha, const double *__restrict__ A, int64_t lda,
                 const double *__restrict__ B, int64_t ldb, double beta, double *C, int64_t ldc, double *scratch,
-                unsigned *counters) {
+                unsigned *counters, int kmode) {
     constexpr int BM = G::BM, BN = G::BN, STAGES = G::STAGES, MT = G::MT, NT = G::NT, THREADS = G::THREADS;
     extern __shared__ __align__(128) double smem[];
     __shared__ unsigned s_last;
@@ -115,8 +115,14 @@ dgemm_tn_kernel(int M, int N, int K, int k_per_split, double alpha, const double
     const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
     const int S = gridDim.z;
     const bool direct = (S == 1);                    // no split: this CTA owns the final tile
-    const int kz0 = blockIdx.z * k_per_split;
-    const int kz1 = min(K, kz0 + k_per_split);
+    int kz0 = blockIdx.z * k_per_split;
+    int kz1 = min(K, kz0 + k_per_split);
+    // structural zeros the caller declares (kmode, gemm_tn): the tile skips k ranges where its
+    // B columns (bit 1: B(k, j) = 0 for k < j) or A rows (bit 2: A(k, i) = 0 for k < i) are zero,
+    // or B is upper triangular (bit 4: B(k, j) = 0 for k > j)
+    if (kmode & 1) kz0 = max(kz0, j0 & ~(BK - 1));
+    if (kmode & 2) kz0 = max(kz0, i0 & ~(BK - 1));
+    if (kmode & 4) kz1 = min(kz1, j0 + BN);
     const int nkt = kz1 > kz0 ? (kz1 - kz0 + BK - 1) / BK : 0;
 
 #pragma unroll

@@ -48,9 +48,13 @@ inline int64_t gemm_scratch_doubles(int64_t M, int64_t N, int64_t K) {
 // C (row-major, ldc) = alpha * A^T B (+ beta * C): A (K x M), B (K x N) column-major.
 // `scratch` holds gemm_scratch_doubles(M, N, K) doubles; `counters` gemm_tiles(M, N) unsigned
 // zero-initialised words (they are left zero again).  alpha must be nonzero.
+// kmode declares structural zeros the tiles may skip (the compact-WY panels' staircase):
+// GEMM_B_STAIR B(k, j) = 0 for k < j; GEMM_A_STAIR A(k, i) = 0 for k < i; GEMM_B_UPPER
+// B(k, j) = 0 for k > j.  The skipped products are exact zeros, so results are unchanged.
+enum { GEMM_B_STAIR = 1, GEMM_A_STAIR = 2, GEMM_B_UPPER = 4 };
 inline int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
                    int64_t ldb, double beta, double *C, int64_t ldc, double *scratch, unsigned *counters,
-                   cudaStream_t s) {
+                   cudaStream_t s, int kmode = 0) {
     using namespace elpa_b200::gemm;
     if (M <= 0 || N <= 0) return ELPA_B200_OK;
     if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || alpha == 0.0) return ELPA_B200_ERR_ARG;
@@ -68,10 +72,10 @@ inline int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double *
     const dim3 grid{unsigned(tx), unsigned(ty), unsigned(S)};
     if (beta != 0.0)
         dgemm_tn_kernel<GemmCfg, true><<<grid, GemmCfg::THREADS, GemmCfg::SMEM, s>>>(
-            int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb, beta, C, ldc, scratch, counters);
+            int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb, beta, C, ldc, scratch, counters, kmode);
     else
         dgemm_tn_kernel<GemmCfg, false><<<grid, GemmCfg::THREADS, GemmCfg::SMEM, s>>>(
-            int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb, 0.0, C, ldc, scratch, counters);
+            int(M), int(N), int(K), int(kps), alpha, A, lda, B, ldb, 0.0, C, ldc, scratch, counters, kmode);
     return cudaGetLastError() == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
 }
 

@@ -80,7 +80,8 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
     for (int64_t p = 0; rc == ELPA_B200_OK && p < np; p++) {
         const int64_t ld = b2f_ld(n, nbw, P, p);
         const double *vp = Vp + b2f_panel_offset(n, nbw, P, p);
-        rc = gemm_tn(P, P, ld, 1.0, vp, ld, vp, ld, 0.0, G + p * P * P, P, scr, cnt, s);
+        // G_p = V_p^T V_p: column a of V_p is zero above relative row a (the staircase)
+        rc = gemm_tn(P, P, ld, 1.0, vp, ld, vp, ld, 0.0, G + p * P * P, P, scr, cnt, s, GEMM_A_STAIR | GEMM_B_STAIR);
     }
     if (rc == ELPA_B200_OK) {
         static bool attr = cudaFuncSetAttribute(b2f_tfactor, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -95,13 +96,13 @@ int elpa_trans_ev_band_to_full(int64_t n, int64_t nbw, int64_t nev, const double
         b2f_transpose_panel<<<g, 256, 0, s>>>(ld, ld, P, Vp + off, VT);
         if (cudaGetLastError() != cudaSuccess) { rc = ELPA_B200_ERR_CUDA; break; }
         // UT[i*P + c] = -sum_a V[i][a] T[a][c]:  A = V^T (K = a, M = i), B = T (K = a, N = c)
-        rc = gemm_tn(ld, P, P, -1.0, VT, P, T + p * P * P, P, 0.0, UT + off, P, scr, cnt, s);
+        rc = gemm_tn(ld, P, P, -1.0, VT, P, T + p * P * P, P, 0.0, UT + off, P, scr, cnt, s, GEMM_B_UPPER);
     }
     // apply, last panel first:  W^T = Q^T V_p,  Q^T += W^T U_p^T  (rows r0' .. n of Q)
     for (int64_t p = np - 1; rc == ELPA_B200_OK && p >= 0; p--) {
         const int64_t r0 = b2f_origin(nbw, P, p), m = n - r0, ld = b2f_ld(n, nbw, P, p);
         const int64_t off = b2f_panel_offset(n, nbw, P, p);
-        rc = gemm_tn(nev, P, m, 1.0, Q + r0, ldq, Vp + off, ld, 0.0, Wt, P, scr, cnt, s);
+        rc = gemm_tn(nev, P, m, 1.0, Q + r0, ldq, Vp + off, ld, 0.0, Wt, P, scr, cnt, s, GEMM_B_STAIR);
         if (rc == ELPA_B200_OK) rc = gemm_tn(nev, m, P, 1.0, Wt, P, UT + off, P, 1.0, Q + r0, ldq, scr, cnt, s);
     }
     if (cudaFreeAsync(buf, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;

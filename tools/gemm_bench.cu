@@ -57,10 +57,10 @@ void run(const char *name, int M, int N, int K, int S, double beta, int reps, bo
     auto launch = [&](double *c) {
         if (beta != 0.0)
             dgemm_tn_kernel<G, true><<<grid, G::THREADS, G::SMEM>>>(M, N, K, int(kps), -1.0, A, lda, B, ldb, beta, c,
-                                                                    ldc, scr, cnt);
+                                                                    ldc, scr, cnt, 0);
         else
             dgemm_tn_kernel<G, false><<<grid, G::THREADS, G::SMEM>>>(M, N, K, int(kps), -1.0, A, lda, B, ldb, 0.0, c,
-                                                                     ldc, scr, cnt);
+                                                                     ldc, scr, cnt, 0);
     };
     double err = -1;
     if (check) {
