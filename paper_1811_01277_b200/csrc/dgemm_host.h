@@ -32,6 +32,16 @@ inline int gemm_split(int64_t M, int64_t N, int64_t K) {
         const double t = double(waves) * double(per) * step_s + (S > 1 ? double(S + 1) * M * N * 8 / 6e12 : 0.0);
         if (t < best * 0.97) { best = t; bs = S; }
     }
+    // Skinny outputs (under two waves of tiles) measured faster with more, power-of-two slices
+    // than this model predicts: at M = 20000, N = 128 (the NEXT-4 block products) S = 4-8 reaches
+    // 0.88-0.90 of peak for K >= 5000 where the model chose S = 2 (0.83-0.84), and S = 3, 5, 6, 7
+    // lose to 4 and 8 (profiles/r02/gemm_split_sweep_n128_r02.jsonl).  So the split is at least
+    // the power of two nearest ksteps / 80, capped at 8.
+    if (tiles < 2 * slots) {
+        int se = 1;
+        while (se < 8 && double(ksteps) / 80.0 >= 1.5 * se) se *= 2;
+        bs = std::max(bs, se);
+    }
     return bs;
 }
 

@@ -149,7 +149,9 @@ int elpa_generalized_back_transform(int64_t n, int64_t nev, const double *L, int
         const int64_t r0 = b * NB, m = std::min<int64_t>(NB, n - r0), r1 = r0 + m;
         if (r1 < n) rc = gemm_tn(nev, m, n - r1, -1.0, Q + r1, ldq, L + r0 * ldl + r1, ldl, 1.0, Q + r0, ldq, scr, cnt, s);
         // T[c*NB + i] = sum_k Q_b[k][c] Linv[k][i]  (Linv column-major, ld NB)
-        if (rc == ELPA_B200_OK) rc = gemm_tn(nev, m, m, 1.0, Q + r0, ldq, Linv + b * NB * NB, NB, 0.0, T, NB, scr, cnt, s);
+        // (L_bb^{-1} is lower triangular: column i of B is zero above row i)
+        if (rc == ELPA_B200_OK)
+            rc = gemm_tn(nev, m, m, 1.0, Q + r0, ldq, Linv + b * NB * NB, NB, 0.0, T, NB, scr, cnt, s, GEMM_B_STAIR);
         if (rc == ELPA_B200_OK &&
             cudaMemcpy2DAsync(Q + r0, size_t(ldq) * 8, T, size_t(NB) * 8, size_t(m) * 8, size_t(nev),
                               cudaMemcpyDeviceToDevice, s) != cudaSuccess)
