@@ -21,7 +21,7 @@ for (n, nbw, nev) in cfgs:
     eb.prepare(n, nbw, dv, dt, ws)
     fl = eb.credited_flops(n, nbw, nev)
     for sh in [None] + SHAPES:
-        for grid in ([0] if sh is None else [0]):
+        for grid in ([0] if sh is None else [int(g) for g in os.environ.get('GRIDS', '0').split()]):
             opts = None if sh is None else dict(kernel=int(os.environ.get('KERNEL', '2')), depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2], grid_ctas=grid, groups_per_step=sh[3])
             try:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
