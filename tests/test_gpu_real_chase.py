@@ -3,8 +3,8 @@ config"): a random symmetric band matrix (n = 8192, nbw = 64, seed S_3) is bulge
 oracle, its tridiagonal solved (Eq. 5) and the eigenvectors
 back-transformed by the oracle one reflector at a time (Eq. 6) for ALL n columns.
 The CUDA path runs the same inputs through the C-ABI in the launch shapes bench.py uses for
-C3 (the two-group window (1,4,2,2)) and C4 (1,2,2,1), round 1's (1,2,4,1) and (2,2,2,1), and on the
-C4-like 10% eigenvector subset with the automatic choice.  Bars (north_star): max|dQ| / max|Q_oracle| <= 1e-12 over every column, and the
+C3 and C4 (the two-group window (1,4,2,2)), the K2 kernel's thin-stripe shape (1,2,2,1), round 1's
+(1,2,4,1) and (2,2,2,1), and on the C4-like 10% eigenvector subset with the automatic choice.  Bars (north_star): max|dQ| / max|Q_oracle| <= 1e-12 over every column, and the
 eigen-residual ||B Q - Q Lambda||_F / (n ||B||_F) <= 1e-13 of the GPU result."""
 import numpy as np
 import pytest
@@ -63,7 +63,7 @@ def test_real_chase_C3_shape_all_columns(eb, case):
 
 @pytest.mark.parametrize("shape", [(1, 2, 2, 1), (1, 2, 4, 1), (2, 2, 2, 1)])
 def test_real_chase_other_shapes_all_columns(eb, case, shape):
-    """C4's automatic shape (1,2,2,1) and round 1's C3 / C4 shapes on the same real case."""
+    """The K2 kernel's thin-stripe shape (1,2,2,1) and round 1's C3 / C4 shapes on the same real case."""
     D, CW, NCT, K = shape
     got = _run(eb, case, case["Qin"], opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=D, col_warps=CW,
                                                 tiles_per_warp=NCT, groups_per_step=K))
