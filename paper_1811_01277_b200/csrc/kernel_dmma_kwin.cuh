@@ -25,7 +25,11 @@ namespace elpa_b200 {
 // Shared-memory and occupancy arithmetic of the kernel, also used by the host plan (make_plan).
 constexpr int kwin_reg_est(int b8, int NCT, int K) { return 4 * (b8 + K) * NCT + 90; }   // W = b8 + K
 constexpr int kwin_minb(int b8, int CW, int NCT, int K) {
-    const int r = 65536 / (32 * CW * kwin_reg_est(b8, NCT, K));
+    // one-tile warps with two groups per step fit 128 registers without spills (118 at nbw = 64):
+    // four CTAs of four warps per SM instead of three, +4-7% on thin stripes
+    // (profiles/r02/kwin_nct1_minb4_r02.jsonl)
+    const int reg = (NCT == 1 && K == 2) ? 128 : kwin_reg_est(b8, NCT, K);
+    const int r = 65536 / (32 * CW * reg);
     return r < 1 ? 1 : (r > 8 ? 8 : r);
 }
 constexpr size_t kwin_smem(int b8, int CW, int NCT, int K, int stages) {
