@@ -611,15 +611,32 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     // Column blocks of CH eigenvectors stream through NBUF device buffers: H2D on one copy
     // stream, apply on `stream`, D2H on another, so PCIe traffic overlaps the kernel (columns
     // are independent: each block's result is bitwise the unblocked one).
-    // ~6 column blocks (measured 4/6/8/12 at C3: 645/645/648/664 ms; profiles/host_blocks_r01.log;
-    // development override: ELPA_B200_HOST_BLOCKS)
+    // Block schedule [e, m, m, e]: a thin first block (its upload shares PCIe with the reflectors
+    // and delays the first launch) and a thin last one (its download is the exposed tail), two
+    // wide middle blocks (wide stripes run the kernel faster: 29.6 TF/s at 8000 columns against
+    // 28.1 at 3336).  Measured at C3: 6 equal blocks 616 ms, 4 equal 612 ms
+    // (profiles/r02/host_blocks_r02.log).  Below 4000 eigenvectors: two equal blocks.
+    // Development override ELPA_B200_HOST_BLOCKS = k: k equal blocks.
     static const int64_t kBlocks = [] {
         const char *e = getenv("ELPA_B200_HOST_BLOCKS");
-        const int64_t v = e ? atoll(e) : 6;
-        return v >= 1 ? v : 6;
+        const int64_t v = e ? atoll(e) : 0;
+        return v >= 1 ? v : 0;
     }();
-    const int64_t CH = std::max<int64_t>(8, ((nev + kBlocks - 1) / kBlocks + 7) / 8 * 8);
-    const int64_t nblk = (nev + CH - 1) / CH;
+    std::vector<int64_t> bstart;                       // block c = columns [bstart[c], bstart[c+1])
+    auto r8 = [](int64_t x) { return std::max<int64_t>(8, (x + 7) / 8 * 8); };
+    if (kBlocks == 0 && nev >= 4000) {
+        const int64_t e = r8(nev / 10), m = r8((nev - 2 * e + 1) / 2);
+        for (int64_t c0 : {int64_t(0), e, e + m, std::min(nev - e, e + 2 * m)}) bstart.push_back(c0);
+    } else {
+        const int64_t k = kBlocks ? kBlocks : 2;         // few columns: the reflector upload dominates
+        const int64_t ch = r8((nev + k - 1) / k);
+        for (int64_t c0 = 0; c0 < nev; c0 += ch) bstart.push_back(c0);
+    }
+    bstart.push_back(nev);
+    bstart.erase(std::unique(bstart.begin(), bstart.end()), bstart.end());
+    const int64_t nblk = int64_t(bstart.size()) - 1;
+    int64_t CH = 8;
+    for (int64_t c = 0; c < nblk; c++) CH = std::max(CH, bstart[c + 1] - bstart[c]);
     constexpr int NBUF = 3;
     const size_t bqc = size_t(ldq) * CH * 8, bv = size_t(R) * nbw * 8, bt = size_t(R) * 8;
     auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -663,7 +680,7 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     // persistent launch (its last items, with SMs retiring) overlaps the start of the next
     if (rc == ELPA_B200_OK && (cudaStreamWaitEvent(cs2, ev_prep, 0) != cudaSuccess)) rc = ELPA_B200_ERR_CUDA;
     for (int64_t c = 0; rc == ELPA_B200_OK && c < nblk; c++) {
-        const int64_t c0 = c * CH, nc = std::min(CH, nev - c0);
+        const int64_t c0 = bstart[c], nc = bstart[c + 1] - c0;
         double *d = dq[c % NBUF];
         cudaStream_t cs = (c & 1) ? cs2 : s;
         // only the n valid rows of each column cross PCIe, in both directions: a legally sized
