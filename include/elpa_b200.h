@@ -91,7 +91,12 @@ typedef struct {
     int col_warps;       /* CW: warps splitting a work item's column stripe, 0 = auto */
     int tiles_per_warp;  /* NCT: 8-column tiles per warp (1,2,4); an item has CW*NCT tiles */
     int grid_ctas;       /* persistent CTAs to launch, 0 = all co-resident (148 x occupancy) */
-    int groups_per_step; /* K: reflector groups (of 8) per CTA barrier (1,2,4), 0 = auto */
+    int groups_per_step; /* K: reflector groups (of 8) per step, 0 = auto.  DMMA kernel: K = 1 runs
+                            the per-group window (D, CW, NCT from the K = 1 menu); K >= 2 runs the
+                            K-group register window (one depth per item, D = 1; nbw 32 or 64;
+                            (D,CW,NCT,K) in (1,2,2,2) (1,4,2,2) (1,4,1,4) (1,4,1,2) (1,6,2,2)
+                            (1,8,2,2) (1,3,2,2) (1,4,2,3) (1,8,1,2)), the automatic choice at
+                            nbw = 64 (DESIGN.md §5.3 K2b, §6); other combinations: ERR_ARG */
     int fused_k;         /* DFMA kernel only: reflectors fused per group, k = 2, 4, 6 or 8 (0 = 8);
                             must be 0 for the other kernels */
 } elpa_b200_opts;
