@@ -130,11 +130,12 @@ void auto_shape(int64_t ntile, int64_t M, int b8, int &D, int &CW, int &NCT, int
     //   (1,4,2,2) K=2       14.2  22.7  26.7  27.1  29.0  29.9  30.6  |            28.4  29.0
     //   (1,4,1,2) K=2       21.6  24.7  26.5  26.6  27.2  27.3        |            26.4  26.5
     //   round 1's K = 1     19.7  24.3  26.7  27.0  28.1  28.6  29.0  |            27.4  27.9
-    // With four CTAs per SM at 128 registers (kwin_minb) the one-tile warps win below 400 tiles
-    // (profiles/r02/kwin_nct1_minb4_r02.jsonl): 1000 columns 26.0, 2000 27.7, 2500 27.7 TF/s
-    // (thinner stripes need more, narrower items: a stripe's chain of depth passes is the limit).
-    (void)M;
-    if (b8 == 8 && ntile >= 400) { D = 1; CW = 4; NCT = 2; K = 2; }
+    // With four CTAs per SM at 128 registers (kwin_minb) the one-tile warps win below 500 tiles
+    // when the chain of depth passes is short (M <= 600; profiles/r02/kwin_nct1_minb4_r02.jsonl,
+    // kwin_nct1_threshold_r02.jsonl): 1000 columns 26.0, 2000 27.7, 2500 27.7, 3334 28.4 against
+    // 28.0 for (1,4,2,2); even at 4000; behind from 5000 (28.7 vs 29.0).  The n = 60000 shard
+    // (938 depths, 3750 columns) keeps two-tile warps: 28.7 against 26.5.
+    if (b8 == 8 && (ntile >= 500 || M > 600)) { D = 1; CW = 4; NCT = 2; K = 2; }
     else if (b8 == 8) { D = 1; CW = 4; NCT = 1; K = 2; }
     else if (b8 == 4 && ntile < 2000) { D = 4; CW = 2; NCT = 2; }
     else { D = 2; CW = 2; NCT = 2; }   // also the default of the small menu (nbw != 8/16/32/64)
