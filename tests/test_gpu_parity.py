@@ -216,6 +216,30 @@ def test_workspace_cache_off_and_on(eb):
     assert np.array_equal(run_gpu(eb, n, nbw, hv, tau, Q), want)
 
 
+def test_host_entry_block_schedule(eb):
+    """nev >= 4000: the host entry's four-block schedule [nev/10, 0.4 nev, 0.4 nev, nev/10] (thin
+    blocks run one-tile warps, wide ones two-tile warps) agrees with the device-pointer call to
+    rounding (the two shapes sum the dot in different orders), inside NaN guard bands."""
+    import torch
+    from inputs import synthetic_q_torch
+    n, nbw, nev = 4200, 64, 4100
+    R = eb.hh_count(n, nbw)
+    hv, tau = synthetic_reflectors(R, nbw, 23)
+    Q = synthetic_q_torch(n, 0, nev, 24).numpy()
+    dev = run_gpu(eb, n, nbw, hv, tau, Q)
+    G = 4096
+    flat = torch.full((G + nev * n + G,), float("nan"), dtype=torch.float64).pin_memory()
+    view = flat[G:G + nev * n].view(nev, n)
+    view.copy_(torch.from_numpy(Q))
+    eb.trans_ev_tridi_to_band_host(n, nbw, torch.from_numpy(hv).pin_memory(), torch.from_numpy(tau).pin_memory(),
+                                   view)
+    out = flat.numpy()
+    assert np.all(np.isnan(out[:G])) and np.all(np.isnan(out[G + nev * n:]))
+    got = view.numpy()
+    assert np.isfinite(got).all()
+    assert float(np.abs(got - dev).max() / np.abs(dev).max()) <= 1e-13
+
+
 @pytest.mark.parametrize("n,nbw,nev", [(900, 64, 50), (1000, 32, 203), (777, 16, 7)])
 def test_host_entry_point(eb, n, nbw, nev):
     """Host buffers, column blocks pipelined over copy streams: equal to the oracle, and
