@@ -36,11 +36,17 @@ inline int gemm_split(int64_t M, int64_t N, int64_t K) {
     // than this model predicts: at M = 20000, N = 128 (the NEXT-4 block products) S = 4-8 reaches
     // 0.88-0.90 of peak for K >= 5000 where the model chose S = 2 (0.83-0.84), and S = 3, 5, 6, 7
     // lose to 4 and 8 (profiles/r02/gemm_split_sweep_n128_r02.jsonl).  So the split is at least
-    // the power of two nearest ksteps / 80, capped at 8.
+    // the power of two nearest ksteps / 80, capped at 8; and a split the model chose is rounded up
+    // to a power of two (at M = 2000, N = 128, K = 19800: S = 13 0.71, S = 16 0.77 of peak;
+    // profiles/r02/gemm_split_sweep_small_r02.jsonl).
     if (tiles < 2 * slots) {
         int se = 1;
         while (se < 8 && double(ksteps) / 80.0 >= 1.5 * se) se *= 2;
         bs = std::max(bs, se);
+        int p2 = 1;
+        while (p2 < bs && p2 < 16) p2 *= 2;
+        while (p2 > 1 && ksteps / p2 < 8) p2 /= 2;
+        bs = p2;
     }
     return bs;
 }
