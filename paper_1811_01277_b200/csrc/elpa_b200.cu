@@ -612,10 +612,11 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     // Column blocks of CH eigenvectors stream through NBUF device buffers: H2D on one copy
     // stream, apply on `stream`, D2H on another, so PCIe traffic overlaps the kernel (columns
     // are independent: each block's result is bitwise the unblocked one).
-    // Block schedule [e, m, m, e]: a thin first block (its upload shares PCIe with the reflectors
-    // and delays the first launch) and a thin last one (its download is the exposed tail), two
-    // wide middle blocks (wide stripes run the kernel faster: 29.6 TF/s at 8000 columns against
-    // 28.1 at 3336).  Measured at C3: 6 equal blocks 616 ms, 4 equal 612 ms
+    // Block schedule [e, m, e], e = nev/10: a thin first block (its upload shares PCIe with the
+    // reflectors and delays the first launch; its compute covers the wide block's upload) and a
+    // thin last one (its download is the exposed tail; its compute covers the wide block's
+    // download), one wide middle block (wide stripes run the kernel faster: 30.4 TF/s at 16000
+    // columns, 29.6 at 8000, 28.1 at 3336).  Measured at C3: 6 equal blocks 616 ms, 4 equal 612 ms
     // (profiles/r02/host_blocks_r02.log).  Below 4000 eigenvectors: two equal blocks.
     // Development override ELPA_B200_HOST_BLOCKS = k: k equal blocks.
     static const int64_t kBlocks = [] {
@@ -626,8 +627,8 @@ int elpa_trans_ev_tridi_to_band_host(int64_t n, int64_t nbw, int64_t nev, const 
     std::vector<int64_t> bstart;                       // block c = columns [bstart[c], bstart[c+1])
     auto r8 = [](int64_t x) { return std::max<int64_t>(8, (x + 7) / 8 * 8); };
     if (kBlocks == 0 && nev >= 4000) {
-        const int64_t e = r8(nev / 10), m = r8((nev - 2 * e + 1) / 2);
-        for (int64_t c0 : {int64_t(0), e, e + m, std::min(nev - e, e + 2 * m)}) bstart.push_back(c0);
+        const int64_t e = r8(nev / 10);
+        for (int64_t c0 : {int64_t(0), e, nev - e}) bstart.push_back(c0);
     } else {
         const int64_t k = kBlocks ? kBlocks : 2;         // few columns: the reflector upload dominates
         const int64_t ch = r8((nev + k - 1) / k);
