@@ -10,6 +10,7 @@
 #include "geometry.cuh"
 #include "host_common.h"
 #include "kernel_dmma.cuh"
+#include "kernel_dmma_kwin.cuh"
 #include "kernel_zprep.cuh"
 
 using namespace elpa_b200;
@@ -25,6 +26,19 @@ struct ZShape { int D, CW, NZ; };
 #define ELPA_Z_ENTRY(D_, CW_, NZ_) {D_, CW_, NZ_},
 constexpr ZShape kZShapes[] = {ELPA_Z_SHAPES(ELPA_Z_ENTRY)};
 constexpr ZShape kZSmallShapes[] = {ELPA_Z_SMALL_SHAPES(ELPA_Z_ENTRY)};
+
+// The K-group register-window kernel (kernel_dmma_kwin.cuh, KIND_ZMMA): D = 1, one complex tile
+// per warp, K = 2 groups per step; nbw 32 and 64.
+#define ELPA_ZK_SHAPES(X) X(4, 1, 2) X(2, 1, 2) X(8, 1, 2)
+struct ZkShape { int CW, NZ, K; };
+#define ELPA_ZK_ENTRY(CW_, NZ_, K_) {CW_, NZ_, K_},
+constexpr ZkShape kZkShapes[] = {ELPA_ZK_SHAPES(ELPA_ZK_ENTRY)};
+bool zk_compiled(int b8, int D, int CW, int NZ, int K) {
+    if ((b8 != 4 && b8 != 8) || D != 1) return false;
+    for (const ZkShape &s : kZkShapes)
+        if (s.CW == CW && s.NZ == NZ && s.K == K) return true;
+    return false;
+}
 
 bool z_full_menu(int b8) { return b8 == 1 || b8 == 2 || b8 == 4 || b8 == 8; }
 bool z_b8_supported(int64_t nbw) { return nbw % 8 == 0 && nbw >= 8 && nbw <= 128; }
@@ -42,7 +56,7 @@ bool z_shape_compiled(int b8, int D, int CW, int NZ) {
 
 struct ZPlan {
     int kernel = ELPA_B200_KERNEL_REFERENCE;
-    int b8 = 0, D = 1, CW = 1, NZ = 1;
+    int b8 = 0, D = 1, CW = 1, NZ = 1, K = 1;
     int grid_req = 0;
     int64_t items = 0, grid = 1;
     int threads = 128;
@@ -64,7 +78,6 @@ int z_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, ZP
     if (kernel == ELPA_B200_KERNEL_AUTO)
         kernel = z_b8_supported(nbw) ? ELPA_B200_KERNEL_DMMA : ELPA_B200_KERNEL_REFERENCE;
     if (kernel == ELPA_B200_KERNEL_DMMA && !z_b8_supported(nbw)) return ELPA_B200_ERR_ARG;
-    if (o && o->groups_per_step > 1) return ELPA_B200_ERR_ARG;
     p.kernel = kernel;
     if (kernel == ELPA_B200_KERNEL_REFERENCE) {
         p.threads = 128;
@@ -73,6 +86,15 @@ int z_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, ZP
     }
     p.b8 = int(nbw / 8);
     int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NZ = o ? o->tiles_per_warp : 0;
+    int K = (o && o->groups_per_step) ? o->groups_per_step : 0;
+    const int64_t ntile_z = (nev + 7) / 8;
+    if (D == 0 && CW == 0 && NZ == 0 && K == 0 && p.b8 == 8 && ntile_z < 1000) {
+        // thin complex stripes run the two-group register window (kernel_dmma_kwin.cuh):
+        // 2000 columns 29.2 TF/s against 28.3, 5000 30.0 against 29.8; at 20000 the K = 1 kernel
+        // stays ahead, 30.7 against 30.3 (profiles/r02/c64_kwin_r02.jsonl)
+        D = 1; CW = 4; NZ = 1; K = 2;
+    }
+    if (K == 0) K = 1;
     if (D == 0 && CW == 0 && NZ == 0) {
         // (1,4,1) everywhere on the full menu: MEDIUM autotuning with the ring-mode kernel
         // (profiles/autotune_medium_r01_final.jsonl) picks it at C4 (28.2 TF/s; (2,2,2) measured
@@ -80,8 +102,9 @@ int z_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, ZP
         if (z_full_menu(p.b8)) { D = 1; CW = 4; NZ = 1; }
         else { D = 2; CW = 2; NZ = 1; }
     }
-    if (!z_shape_compiled(p.b8, D, CW, NZ)) return ELPA_B200_ERR_ARG;
-    p.D = D; p.CW = CW; p.NZ = NZ;
+    const bool kwin = K >= 2;
+    if (kwin ? !zk_compiled(p.b8, D, CW, NZ, K) : !z_shape_compiled(p.b8, D, CW, NZ)) return ELPA_B200_ERR_ARG;
+    p.D = D; p.CW = CW; p.NZ = NZ; p.K = K;
     p.grid_req = o ? o->grid_ctas : 0;
     if (p.grid_req < 0) return ELPA_B200_ERR_ARG;
     const int64_t M = num_depths(n, nbw);
@@ -90,7 +113,8 @@ int z_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, ZP
     p.items = nx * ((M + D - 1) / D);
     p.grid = p.items;
     p.threads = 32 * D * CW;
-    p.smem = z_smem(p.b8, D, CW, NZ);
+    p.smem = kwin ? kwin_smem(p.b8, CW, 2 * NZ, K, kwin_stages(p.b8, CW, 2 * NZ, K, KIND_ZMMA), KIND_ZMMA)
+                  : z_smem(p.b8, D, CW, NZ);
     if (p.smem > size_t(smem_optin())) return ELPA_B200_ERR_ARG;
     p.ws_bytes = (M > 0) ? total_groups(n, p.b8, M) * blob_doubles(p.b8 + 1, 2) * 8 : 0;
     return ELPA_B200_OK;
@@ -130,6 +154,30 @@ int z_launch_shape(const ZPlan &p, int64_t n, int64_t nev, const double *ws, dou
     return rc;
 }
 
+template <int B8, int CW, int NZ, int K>
+int zk_launch_shape(const ZPlan &p, int64_t n, int64_t nev, const double *ws, double *Q, int64_t ldq, cudaStream_t s) {
+    using Cfg = KwinCfg<B8, CW, 2 * NZ, K, KIND_ZMMA>;
+    auto kern = apply_dmma_kwin_kernel<B8, CW, 2 * NZ, K, KIND_ZMMA>;
+    int per_sm = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS, Cfg::SMEM) != cudaSuccess ||
+        per_sm < 1)
+        return fail_cuda();
+    int64_t grid = int64_t(per_sm) * sm_count();
+    if (p.grid_req > 0 && p.grid_req < grid) grid = p.grid_req;
+    if (grid > p.items) grid = p.items;
+    uint64_t *prog = nullptr;
+    const size_t pbytes = size_t(p.items * CW + 1) * 8;   // one word per (item, column warp) + counter
+    if (lib_malloc_async(reinterpret_cast<void **>(&prog), pbytes, s) != cudaSuccess) return fail_cuda();
+    int rc = cudaMemsetAsync(prog, 0, pbytes, s) == cudaSuccess ? ELPA_B200_OK : ELPA_B200_ERR_CUDA;
+    if (rc == ELPA_B200_OK) {
+        kern<<<unsigned(grid), Cfg::THREADS, Cfg::SMEM, s>>>(n, nev, ws, Q, ldq, prog, kwin_pub_period((nev + 7) / 8));
+        if (cudaGetLastError() != cudaSuccess) rc = ELPA_B200_ERR_CUDA;
+    }
+    if (cudaFreeAsync(prog, s) != cudaSuccess && rc == ELPA_B200_OK) rc = ELPA_B200_ERR_CUDA;
+    return rc;
+}
+
 template <int B8>
 int z_run_b8(const ZPlan &p, int64_t n, int64_t nev, const double *hh_v, const double *hh_tau, double *ws, double *Q,
              int64_t ldq, cudaStream_t s) {
@@ -137,6 +185,13 @@ int z_run_b8(const ZPlan &p, int64_t n, int64_t nev, const double *hh_v, const d
     const int64_t G0 = groups_at_depth(n, B8, 0);
     prep_zmma_kernel<B8><<<dim3(unsigned((G0 + 1) / 2), unsigned(M)), 64, 0, s>>>(n, hh_v, hh_tau, ws);
     if (cudaGetLastError() != cudaSuccess) return ELPA_B200_ERR_CUDA;
+    if constexpr (B8 == 4 || B8 == 8) {
+#define ELPA_ZK_CASE(CW_, NZ_, K_) \
+        if (p.K == K_ && p.CW == CW_ && p.NZ == NZ_) return zk_launch_shape<B8, CW_, NZ_, K_>(p, n, nev, ws, Q, ldq, s);
+        ELPA_ZK_SHAPES(ELPA_ZK_CASE)
+#undef ELPA_ZK_CASE
+    }
+    if (p.K != 1) return ELPA_B200_ERR_ARG;
 #define ELPA_Z_CASE(D_, CW_, NZ_) \
     if (p.D == D_ && p.CW == CW_ && p.NZ == NZ_) return z_launch_shape<B8, D_, CW_, NZ_>(p, n, nev, ws, Q, ldq, s);
     if constexpr (B8 == 1 || B8 == 2 || B8 == 4 || B8 == 8) {
@@ -205,8 +260,8 @@ int elpa_b200_describe_c64(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_
     int rc = z_make_plan(n, nbw, nev, opts, p);
     if (rc != ELPA_B200_OK) return rc;
     if (buf && buflen)
-        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NZ=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
-                 p.kernel == ELPA_B200_KERNEL_DMMA ? "zmma" : "reference_c64", p.b8, p.D, p.CW, p.NZ,
+        snprintf(buf, buflen, "kernel=%s b8=%d D=%d CW=%d NZ=%d K=%d items=%lld grid_req=%d block=%d smem=%zu ws=%lld",
+                 p.kernel == ELPA_B200_KERNEL_DMMA ? "zmma" : "reference_c64", p.b8, p.D, p.CW, p.NZ, p.K,
                  (long long)p.items, p.grid_req, p.threads, p.smem, (long long)p.ws_bytes);
     if (hh_total(n, nbw) == 0 || nev == 0) return 0;
     return p.kernel == ELPA_B200_KERNEL_REFERENCE ? 1 : 2;

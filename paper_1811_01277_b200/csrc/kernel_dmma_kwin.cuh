@@ -24,24 +24,25 @@ namespace elpa_b200 {
 
 // Shared-memory and occupancy arithmetic of the kernel, also used by the host plan (make_plan).
 constexpr int kwin_reg_est(int b8, int NCT, int K) { return 4 * (b8 + K) * NCT + 90; }   // W = b8 + K
-constexpr int kwin_minb(int b8, int CW, int NCT, int K) {
+constexpr int kwin_minb(int b8, int CW, int NCT, int K, int kind = KIND_DMMA) {
     // one-tile warps with two groups per step fit 128 registers without spills (118 at nbw = 64):
     // four CTAs of four warps per SM instead of three, +4-7% on thin stripes
     // (profiles/r02/kwin_nct1_minb4_r02.jsonl)
-    const int reg = (NCT == 1 && K == 2) ? 128 : kwin_reg_est(b8, NCT, K);
+    const int reg = (kind == KIND_DMMA && NCT == 1 && K == 2) ? 128 : kwin_reg_est(b8, NCT, K);
     const int r = 65536 / (32 * CW * reg);
     return r < 1 ? 1 : (r > 8 ? 8 : r);
 }
-constexpr size_t kwin_smem(int b8, int CW, int NCT, int K, int stages) {
-    return size_t(stages) * K * 128 * (b8 + 1) * 8          // fragment ring: stages x K blobs
+constexpr size_t kwin_smem(int b8, int CW, int NCT, int K, int stages, int kind = KIND_DMMA) {
+    return size_t(stages) * K * (kind == KIND_ZMMA ? 256 : 128) * (b8 + 1) * 8   // ring: stages x K blobs
            + size_t(2) * K * CW * NCT * 64 * 8               // Q intake, double-buffered
            + size_t(2) * stages * 8 + 16;                    // mbarriers + item slot
 }
 // Fragment ring depth: 3 stages where they fit the register-limited CTA count (228 KB per SM, 1 KB
 // reserved per CTA), else 2.  Measured at C3 (1,4,2,2): 2 -> 3 stages 30.42 -> 30.60 TF/s; a
 // shape that would lose a CTA per SM keeps 2 ((1,2,2,2): 28.4 -> 23.7 with 3).
-constexpr int kwin_stages(int b8, int CW, int NCT, int K) {
-    return size_t(kwin_minb(b8, CW, NCT, K)) * (kwin_smem(b8, CW, NCT, K, 3) + 1024) <= size_t(233472) ? 3 : 2;
+constexpr int kwin_stages(int b8, int CW, int NCT, int K, int kind = KIND_DMMA) {
+    return size_t(kwin_minb(b8, CW, NCT, K, kind)) * (kwin_smem(b8, CW, NCT, K, 3, kind) + 1024) <= size_t(233472)
+               ? 3 : 2;
 }
 
 // compile-time loop: f(integral_constant<int, I>) for I = I0 .. I1-1
@@ -53,18 +54,21 @@ __device__ __forceinline__ void static_for_kwin(F &&f) {
     }
 }
 
-template <int B8, int CW, int NCT, int K>
+// KIND_ZMMA: the complex Hermitian variant (NEXT-3), NCT real tiles = NCT/2 complex tiles as
+// (Re, Im) pairs, ZmmaGroup's arithmetic (kernel_dmma.cuh) on the same window.
+template <int B8, int CW, int NCT, int K, int KIND = KIND_DMMA>
 struct KwinCfg {
     static constexpr int LAM = B8 + 1;
+    static constexpr int ZF = (KIND == KIND_ZMMA) ? 2 : 1; // real tiles per (complex) tile
     static constexpr int W = LAM + K - 1;                 // window chunks
-    static constexpr int BLOB = 128 * LAM;                // doubles per prepared group (DMMA layout)
+    static constexpr int BLOB = 128 * ZF * LAM;           // doubles per prepared group
     static constexpr int THREADS = 32 * CW;
-    static constexpr int T = CW * NCT;                    // 8-column tiles per work item
-    static constexpr int STAGES = kwin_stages(B8, CW, NCT, K);   // fragment ring (K blobs per stage)
+    static constexpr int T = CW * NCT / ZF;               // 8-column tiles per work item
+    static constexpr int STAGES = kwin_stages(B8, CW, NCT, K, KIND);   // fragment ring (K blobs per stage)
     static constexpr size_t SMEM_BLOBS = size_t(STAGES) * K * BLOB * sizeof(double);
     static constexpr size_t SMEM_INTAKE = size_t(2) * K * CW * NCT * 64 * sizeof(double);
-    static constexpr size_t SMEM = kwin_smem(B8, CW, NCT, K, STAGES);
-    static constexpr int MINB = kwin_minb(B8, CW, NCT, K);
+    static constexpr size_t SMEM = kwin_smem(B8, CW, NCT, K, STAGES, KIND);
+    static constexpr int MINB = kwin_minb(B8, CW, NCT, K, KIND);
 };
 
 // One compact-WY group (DmmaGroup's arithmetic) on window chunks [OFF, OFF + LAM) of q[NCT][W].
@@ -109,11 +113,72 @@ __device__ __forceinline__ void dmma_group_at(double2 (&q)[NCT][W], const double
     }
 }
 
-template <int B8, int CW, int NCT, int K>
-__global__ void __launch_bounds__(KwinCfg<B8, CW, NCT, K>::THREADS, KwinCfg<B8, CW, NCT, K>::MINB)
+// One complex group (ZmmaGroup's arithmetic, kernel_dmma.cuh) on window chunks [OFF, OFF + LAM):
+// q[2u] = Re, q[2u+1] = Im of complex tile u.
+template <int LAM, int NCT, int W, int OFF>
+__device__ __forceinline__ void zmma_group_at(double2 (&q)[NCT][W], const double *blob, int lane) {
+    constexpr int NZ = NCT / 2;
+    const double2 *dUr = reinterpret_cast<const double2 *>(blob);
+    const double2 *dUi = dUr + 32 * LAM;
+    const double2 *uVr = dUr + 64 * LAM;
+    const double2 *uVi = dUr + 96 * LAM;
+    double2 ya[NZ], yb[NZ], yc[NZ], yd[NZ];                // Qr.Ur, Qi.Ui, Qi.Ur, Qr.Ui
+#pragma unroll
+    for (int u = 0; u < NZ; u++) ya[u] = yb[u] = yc[u] = yd[u] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < LAM; i++) {
+        const double2 ur = dUr[i * 32 + lane], ui = dUi[i * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < NZ; u++) {
+            const double2 qr = q[2 * u][OFF + i], qi = q[2 * u + 1][OFF + i];
+            dmma(ya[u].x, ya[u].y, qr.x, ur.x);
+            dmma(yb[u].x, yb[u].y, qi.x, ui.x);
+            dmma(yc[u].x, yc[u].y, qi.x, ur.x);
+            dmma(yd[u].x, yd[u].y, qr.x, ui.x);
+            dmma(ya[u].x, ya[u].y, qr.y, ur.y);
+            dmma(yb[u].x, yb[u].y, qi.y, ui.y);
+            dmma(yc[u].x, yc[u].y, qi.y, ur.y);
+            dmma(yd[u].x, yd[u].y, qr.y, ui.y);
+        }
+    }
+    double2 wr[NZ], wi[NZ], nwi[NZ];
+#pragma unroll
+    for (int u = 0; u < NZ; u++) {
+        wr[u] = make_double2(ya[u].x + yb[u].x, ya[u].y + yb[u].y);
+        wi[u] = make_double2(yc[u].x - yd[u].x, yc[u].y - yd[u].y);
+        nwi[u] = make_double2(-wi[u].x, -wi[u].y);
+    }
+#pragma unroll
+    for (int i = 0; i < LAM; i++) {
+        const double2 vr = uVr[i * 32 + lane], vi = uVi[i * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < NZ; u++) {
+            double2 &qr = q[2 * u][OFF + i];
+            double2 &qi = q[2 * u + 1][OFF + i];
+            dmma(qr.x, qr.y, wr[u].x, vr.x);
+            dmma(qi.x, qi.y, wr[u].x, vi.x);
+            dmma(qr.x, qr.y, wr[u].y, vr.y);
+            dmma(qi.x, qi.y, wr[u].y, vi.y);
+            dmma(qr.x, qr.y, nwi[u].x, vi.x);
+            dmma(qi.x, qi.y, wi[u].x, vr.x);
+            dmma(qr.x, qr.y, nwi[u].y, vi.y);
+            dmma(qi.x, qi.y, wi[u].y, vr.y);
+        }
+    }
+}
+
+template <int KIND, int LAM, int NCT, int W, int OFF>
+__device__ __forceinline__ void kwin_group_at(double2 (&q)[NCT][W], const double *blob, int lane) {
+    if constexpr (KIND == KIND_ZMMA) zmma_group_at<LAM, NCT, W, OFF>(q, blob, lane);
+    else dmma_group_at<LAM, NCT, W, OFF>(q, blob, lane);
+}
+
+template <int B8, int CW, int NCT, int K, int KIND = KIND_DMMA>
+__global__ void __launch_bounds__(KwinCfg<B8, CW, NCT, K, KIND>::THREADS, KwinCfg<B8, CW, NCT, K, KIND>::MINB)
 apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ blobs, double *Q, int64_t ldq,
                        uint64_t *prog, int pub_period) {
-    using Cfg = KwinCfg<B8, CW, NCT, K>;
+    using Cfg = KwinCfg<B8, CW, NCT, K, KIND>;
+    constexpr int ZF = Cfg::ZF;
     constexpr int LAM = Cfg::LAM, W = Cfg::W, BLOB = Cfg::BLOB, S = Cfg::STAGES, T = Cfg::T;
     constexpr int B = 8 * B8;
     constexpr int AHEAD = S - 1;                           // the issuer waits only for its own last step
@@ -161,10 +226,10 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
         uint32_t okmask = 0;
 #pragma unroll
         for (int t = 0; t < NCT; t++) {
-            const int tile = x * T + cw * NCT + t;
+            const int tile = x * T + cw * (NCT / ZF) + t / ZF;
             const int c = tile * 8 + (lane >> 2);
             if (tile < tile_end && c < nev) okmask |= 1u << t;
-            qcol[t] = Q + int64_t(min(c, nev - 1)) * ldq;
+            qcol[t] = Q + int64_t(ZF) * int64_t(min(c, nev - 1)) * ldq;
         }
         const int G = int(groups_at_depth(n64, B8, p));
         const int NT = G;                                  // group-times of this item
@@ -218,7 +283,12 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
 #pragma unroll
             for (int j = 0; j < K; j++) {
                 const int c = top + j;
-                if (okmask == kAllTiles && c >= 0 && 8 * c + 8 <= n) {
+                if constexpr (ZF == 2) {
+#pragma unroll
+                    for (int t = 0; t < NCT; t += 2)
+                        zload_pair_async(&sintake[islot(st & 1, j, t)], &sintake[islot(st & 1, j, t + 1)], qcol[t],
+                                         (okmask >> t) & 1, n, 8 * c + rsub);
+                } else if (okmask == kAllTiles && c >= 0 && 8 * c + 8 <= n) {
 #pragma unroll
                     for (int t = 0; t < NCT; t++)
                         cp_async16_zfill(&sintake[islot(st & 1, j, t)], qcol[t] + 8 * c + rsub, 16u);
@@ -231,6 +301,11 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
             cp_async_commit();
         };
         auto store_tiles = [&](const double2 *v, int r) {  // v[t], t < NCT
+            if constexpr (ZF == 2) {
+#pragma unroll
+                for (int t = 0; t < NCT; t += 2) zstore_pair(qcol[t], (okmask >> t) & 1, n, r, v[t], v[t + 1]);
+                return;
+            }
             if (okmask == kAllTiles && r >= 0 && r + 2 <= n) {
 #pragma unroll
                 for (int t = 0; t < NCT; t++) *reinterpret_cast<double2 *>(qcol[t] + r) = v[t];
@@ -244,9 +319,16 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
         const int T0 = C0 - (K - 1);
         await_chunk(T0);
 #pragma unroll
-        for (int i = 0; i < W; i++)
+        for (int i = 0; i < W; i++) {
+            if constexpr (ZF == 2) {
 #pragma unroll
-            for (int t = 0; t < NCT; t++) q[t][i] = load_pair(qcol[t], (okmask >> t) & 1, n, 8 * (T0 + i) + rsub);
+                for (int t = 0; t < NCT; t += 2)
+                    zload_pair(qcol[t], (okmask >> t) & 1, n, 8 * (T0 + i) + rsub, q[t][i], q[t + 1][i]);
+            } else {
+#pragma unroll
+                for (int t = 0; t < NCT; t++) q[t][i] = load_pair(qcol[t], (okmask >> t) & 1, n, 8 * (T0 + i) + rsub);
+            }
+        }
         if (nsteps > 1) intake(0);
 
         int st = 0;
@@ -259,12 +341,12 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
             if (st * K + K <= NT) {                        // a full step: one basic block, so the
                 static_for_kwin<0, K>([&](auto jc) {       // groups' DMMAs interleave (+1.7% at C3)
                     constexpr int j = decltype(jc)::value;
-                    dmma_group_at<LAM, NCT, W, K - 1 - j>(q, sb + j * BLOB, lane);
+                    kwin_group_at<KIND, LAM, NCT, W, K - 1 - j>(q, sb + j * BLOB, lane);
                 });
             } else {                                       // the item's last step, NT % K groups
                 static_for_kwin<0, K>([&](auto jc) {
                     constexpr int j = decltype(jc)::value;
-                    if (st * K + j < NT) dmma_group_at<LAM, NCT, W, K - 1 - j>(q, sb + j * BLOB, lane);
+                    if (st * K + j < NT) kwin_group_at<KIND, LAM, NCT, W, K - 1 - j>(q, sb + j * BLOB, lane);
                 });
             }
             __syncwarp();
@@ -289,8 +371,16 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
 #pragma unroll
                     for (int i = W - 1; i >= K; i--) q[t][i] = q[t][i - K];
                 }
+                if constexpr (ZF == 2) {
+                    if (t & 1) {                           // the (Re, Im) pair, split at its odd member
 #pragma unroll
-                for (int j = 0; j < K; j++) q[t][j] = sintake[islot(st & 1, j, t)];
+                        for (int j = 0; j < K; j++)
+                            zsplit(sintake[islot(st & 1, j, t - 1)], sintake[islot(st & 1, j, t)], q[t - 1][j], q[t][j]);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < K; j++) q[t][j] = sintake[islot(st & 1, j, t)];
+                }
             }
             if (pub) {                                     // per-warp word: no CTA barrier
                 __syncwarp();

@@ -67,6 +67,33 @@ def test_complex_dmma_all_shapes(eb, shape, nbw):
         assert np.array_equal(got[:, n:], Q[:, n:])
 
 
+KWIN_SHAPES = [(4, 1, 2), (2, 1, 2), (8, 1, 2)]
+
+
+@pytest.mark.parametrize("shape", KWIN_SHAPES)
+@pytest.mark.parametrize("nbw", [32, 64])
+def test_complex_kwin_shapes(eb, shape, nbw):
+    """The K-group register-window kernel on complex tiles (KIND_ZMMA): D = 1, two groups per
+    step; grids of 1 and 3 CTAs exercise the per-warp progress words across items."""
+    CW, NZ, K = shape
+    for n, nev in ((301, 45), (130, 129), (17, 17)):
+        hv, tau, s, L, Q = zcase(n, nbw, nev, nbw * 7 + CW + n, ldq=n + 2)
+        want = oracle.apply_c(hv, tau, s, L, Q)
+        for grid in (0, 1, 3):
+            got = runz(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=1, col_warps=CW,
+                                                          tiles_per_warp=NZ, grid_ctas=grid, groups_per_step=K))
+            assert _rel(got[:, :n], want[:, :n]) <= TOL, (shape, n, grid)
+            assert np.array_equal(got[:, n:], Q[:, n:])
+
+
+def test_complex_kwin_rejects_unsupported(eb):
+    n, nbw, nev = 100, 16, 10
+    hv, tau, s, L, Q = zcase(n, nbw, nev, 3)
+    with pytest.raises(eb.ElpaB200Error):
+        runz(eb, n, nbw, hv, tau, Q, opts=dict(kernel=eb.KERNEL_DMMA, depth_warps=1, col_warps=4, tiles_per_warp=1,
+                                               groups_per_step=2))
+
+
 @pytest.mark.parametrize("nbw", [24, 40, 72, 128])
 def test_complex_nbw_range(eb, nbw):
     n, nev = 400, 50
@@ -102,7 +129,8 @@ def test_complex_guard_bands(eb):
     big = torch.full((G + nev * ldq + G,), complex(float("nan"), float("nan")), dtype=torch.complex128, device="cuda")
     big[G:G + nev * ldq] = torch.from_numpy(Q.reshape(-1)).cuda()
     dq = big[G:G + nev * ldq].view(nev, ldq)
-    for opts in (None, dict(kernel=eb.KERNEL_DMMA, depth_warps=2, col_warps=2, tiles_per_warp=1)):
+    for opts in (None, dict(kernel=eb.KERNEL_DMMA, depth_warps=2, col_warps=2, tiles_per_warp=1),
+                 dict(kernel=eb.KERNEL_DMMA, depth_warps=1, col_warps=4, tiles_per_warp=1, groups_per_step=2)):
         dq.copy_(torch.from_numpy(Q).cuda())
         eb.trans_ev_tridi_to_band(n, nbw, torch.from_numpy(hv).cuda(), torch.from_numpy(tau).cuda(), dq, opts=opts)
         torch.cuda.synchronize()

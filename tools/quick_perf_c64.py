@@ -23,7 +23,8 @@ for (n, nbw, nev) in cfgs:
         dq[a:a + 2000] = torch.from_numpy(synthetic_q_c_np(n, a, min(nev, a + 2000), 2)).cuda()
     fl = 4 * eb.credited_flops(n, nbw, nev)
     for sh in [None] + SHAPES:
-        opts = None if sh is None else dict(kernel=eb.KERNEL_DMMA, depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2])
+        opts = None if sh is None else dict(kernel=eb.KERNEL_DMMA, depth_warps=sh[0], col_warps=sh[1], tiles_per_warp=sh[2],
+                                            groups_per_step=sh[3] if len(sh) > 3 else 1)
         try:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             eb.trans_ev_tridi_to_band(n, nbw, dv, dt, dq, opts=opts); torch.cuda.synchronize()
