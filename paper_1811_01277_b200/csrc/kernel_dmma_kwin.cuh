@@ -16,9 +16,6 @@
 #pragma once
 #include "kernel_dmma.cuh"
 
-#ifndef KWIN_ABL
-#define KWIN_ABL 0      // development ablation mask (wrong results; timing only): 0 in the product
-#endif
 
 namespace elpa_b200 {
 
@@ -260,7 +257,7 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
 
         uint32_t seen = 0;
         auto await_chunk = [&](int c) {                    // chunk c final from depth p-1
-            if (p == 0 || c < 0 || (KWIN_ABL & 8)) return;
+            if (p == 0 || c < 0) return;
             const uint32_t need = uint32_t(C0 + 2 - c);
             if (seen >= need) return;
             if (lane == 0) {
@@ -279,7 +276,6 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
         auto intake = [&](int st) {
             const int top = C0 - (st + 1) * K - (K - 1);
             await_chunk(top);
-            if (KWIN_ABL & 2) { cp_async_commit(); return; }
 #pragma unroll
             for (int j = 0; j < K; j++) {
                 const int c = top + j;
@@ -359,18 +355,16 @@ apply_dmma_kwin_kernel(int64_t n64, int64_t nev64, const double *__restrict__ bl
                 double2 bot[NCT];
 #pragma unroll
                 for (int t = 0; t < NCT; t++) bot[t] = q[t][W - K + jj];
-                if (!(KWIN_ABL & 1)) store_tiles(bot, 8 * (tst + W - K + jj) + rsub);
+                store_tiles(bot, 8 * (tst + W - K + jj) + rsub);
             }
-            const bool pub = (KWIN_ABL & 32) ? false : pub_step(st);
+            const bool pub = pub_step(st);
             if (pub) __threadfence();                      // this lane's stores, before the warp's release
             // slide by K chunks; the new top chunks arrived during this step
             if (st + 1 < nsteps - 1) cp_async_wait<1>(); else cp_async_wait<0>();
 #pragma unroll
             for (int t = 0; t < NCT; t++) {
-                if (!(KWIN_ABL & 16)) {
 #pragma unroll
-                    for (int i = W - 1; i >= K; i--) q[t][i] = q[t][i - K];
-                }
+                for (int i = W - 1; i >= K; i--) q[t][i] = q[t][i - K];
                 if constexpr (ZF == 2) {
                     if (t & 1) {                           // the (Re, Im) pair, split at its odd member
 #pragma unroll
