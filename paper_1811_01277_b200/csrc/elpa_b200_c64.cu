@@ -237,6 +237,12 @@ int elpa_b200_host::c64_shape_menu(int b8, int (*out)[4], int max) {
     if (!z_b8_supported(8 * int64_t(b8))) return 0;
     if (z_full_menu(b8)) add(kZShapes, int(sizeof(kZShapes) / sizeof(kZShapes[0])));
     else add(kZSmallShapes, int(sizeof(kZSmallShapes) / sizeof(kZSmallShapes[0])));
+    if (b8 == 4 || b8 == 8)                              // the register-window shapes (K = 2)
+        for (const ZkShape &z : kZkShapes)
+            if (k < max) {
+                out[k][0] = 1; out[k][1] = z.CW; out[k][2] = z.NZ; out[k][3] = z.K;
+                k++;
+            }
     return k;
 }
 
