@@ -303,7 +303,7 @@ int elpa_b200_describe_f32(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_
  *   oracle); depth_warps D, col_warps CW, tiles_per_warp = complex 8-column tiles per warp;
  *   groups_per_step 0 (auto), 1, or 2 with D = 1, NZ = 1, CW in {2, 4, 8} at nbw 32 or 64 (the
  *   K-group register-window kernel on complex tiles; the automatic choice below 8000 eigenvectors
- *   at nbw = 64); other combinations: ERR_ARG.  Asynchronous on `stream`.
+ *   at nbw 32 and 64); other combinations: ERR_ARG.  Asynchronous on `stream`.
  * ------------------------------------------------------------------------------------- */
 int elpa_trans_ev_tridi_to_band_c64(int64_t n, int64_t nbw, int64_t nev, const double *hh_v, const double *hh_tau,
                                     double *Q, int64_t ldq, elpa_b200_stream_t stream, const elpa_b200_opts *opts);

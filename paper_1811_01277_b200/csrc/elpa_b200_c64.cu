@@ -88,10 +88,11 @@ int z_make_plan(int64_t n, int64_t nbw, int64_t nev, const elpa_b200_opts *o, ZP
     int D = o ? o->depth_warps : 0, CW = o ? o->col_warps : 0, NZ = o ? o->tiles_per_warp : 0;
     int K = (o && o->groups_per_step) ? o->groups_per_step : 0;
     const int64_t ntile_z = (nev + 7) / 8;
-    if (D == 0 && CW == 0 && NZ == 0 && K == 0 && p.b8 == 8 && ntile_z < 1000) {
+    if (D == 0 && CW == 0 && NZ == 0 && K == 0 && (p.b8 == 8 || p.b8 == 4) && ntile_z < 1000) {
         // thin complex stripes run the two-group register window (kernel_dmma_kwin.cuh):
         // 2000 columns 29.2 TF/s against 28.3, 5000 30.0 against 29.8; at 20000 the K = 1 kernel
-        // stays ahead, 30.7 against 30.3 (profiles/r02/c64_kwin_r02.jsonl)
+        // stays ahead, 30.7 against 30.3 (profiles/r02/c64_kwin_r02.jsonl); nbw = 32: C2 25.9
+        // against 24.6, 20000 x 2000 26.2 against 24.9 (c64_kwin_nbw32_r02.log)
         D = 1; CW = 4; NZ = 1; K = 2;
     }
     if (K == 0) K = 1;
